@@ -1,0 +1,124 @@
+/*
+ * zeppelin_b200.h — C ABI of the B200 (sm_100a) per-layer hot path of Zeppelin
+ * (arXiv 2509.21841): the varlen / ring-round causal attention engine and the
+ * attention<->linear remapping layer.
+ *
+ * The reference (`/root/reference/pkg/src/varlenplan`) is a pure-Python cost
+ * model: it counts causal (q,k) pairs and KV tokens but never computes them.
+ * Each entry point below is the device execution of one thing the reference
+ * only charges a cost for:
+ *
+ *   zp_attn_fwd        LocalTask / RingRound compute
+ *                        attention_engine.py:113-141  (visible_pairs: mask semantics)
+ *                        attention_engine.py:229-244  (_ring_schedule: src=(i-r)%g)
+ *                        attention_engine.py:260-265  (LocalTask: whole-sequence causal)
+ *                        simulator.py:142-148,181-187 (where the cost model charges it)
+ *   zp_copy_rows       ring KV pack (held KV set of a ring position) and the
+ *                      remap kept-row/tail copies
+ *                        attention_engine.py:247-251  (KV rotates i -> i+1)
+ *                        remapping.py:187-245         (transfer matrix M rows)
+ *   zp_remap_push      fused remap: rows of M[i][j] stored straight into peer
+ *                      buffers over NVLink, then a signal flag per (sender,receiver)
+ *                        remapping.py:187-255, simulator.py:282-302,336-347
+ *
+ * Conventions: all pointers are device pointers (except where noted); the
+ * library never allocates device memory; every call is asynchronous on the
+ * given cudaStream_t (passed as void*).  Return 0 on success or a negative
+ * ZP_E* code; zp_last_error() returns a static description of the last error.
+ * There is no CPU fallback: without an sm_100a device every call fails.
+ */
+#ifndef ZEPPELIN_B200_H
+#define ZEPPELIN_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define ZP_API __attribute__((visibility("default")))
+#else
+#define ZP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ZP_OK 0
+#define ZP_EINVAL (-1)   /* bad argument / unsupported shape */
+#define ZP_ETMA (-2)     /* tensor-map encode failed */
+#define ZP_ECUDA (-3)    /* CUDA runtime error (launch, attribute, ...) */
+#define ZP_ENODEV (-4)   /* no sm_100 device */
+
+/* One attention work item: a tile of <=128 query rows of one sequence
+ * fragment (contiguous global positions), for a PAIR of query heads
+ * (2*head_pair, 2*head_pair+1) that share one KV head (GQA group size even).
+ * The item attends to `seg_count` KV segments starting at `seg_begin`. */
+typedef struct zp_attn_item {
+  int32_t q_row0;     /* physical row of the first query row in q/o */
+  int32_t q_pos0;     /* global in-sequence position of that row */
+  int32_t q_len;      /* valid rows, 1..128 */
+  int32_t head_pair;  /* query heads 2*head_pair and 2*head_pair+1 */
+  int32_t seg_begin;  /* index into the KV segment table */
+  int32_t seg_count;  /* number of KV segments (same sequence) */
+  int32_t state_row0; /* row of this tile in the ring partial-state buffers */
+  int32_t flags;      /* ZP_ITEM_* */
+} zp_attn_item;
+
+/* A contiguous run of KV rows of one sequence: rows [row0,row0+len) of k/v
+ * hold global positions [pos0, pos0+len). */
+typedef struct zp_kv_seg {
+  int32_t row0;
+  int32_t pos0;
+  int32_t len;
+  int32_t reserved;
+} zp_kv_seg;
+
+#define ZP_ITEM_LOAD_STATE 1  /* resume from (m, l, O_acc) partial state */
+#define ZP_ITEM_STORE_STATE 2 /* write partial state instead of final O/LSE */
+
+/* Causal flash attention over a work-item list (bf16 in, fp32 accumulate).
+ * q: [q_rows, hq, 128] bf16; k, v: [kv_rows, hkv, 128] bf16 with row stride
+ * kv_row_stride elements (>= hkv*128; lets K and V live interleaved in one
+ * ring buffer); o: [q_rows, hq, 128] bf16; lse: [hq, lse_stride] fp32 (natural
+ * log).  Mask: key position <= query position (global in-sequence positions).
+ * state_o: [state_rows, hq, 128] fp32 unnormalised accumulator, state_ml:
+ * [2, hq, state_rows] fp32 (running max in log2 units, running sum); only
+ * touched by items carrying ZP_ITEM_*_STATE.  Items must be device-resident. */
+ZP_API int zp_attn_fwd(const void* q, const void* k, const void* v, int q_rows, int kv_rows,
+                int kv_row_stride, int hq, int hkv, int head_dim, void* o, float* lse,
+                int lse_stride, const zp_attn_item* items, int n_items, const zp_kv_seg* segs,
+                float* state_o, float* state_ml, int state_rows, float softmax_scale,
+                void* stream);
+
+/* Row-range copy with 16-byte vector loads/stores.  For each range i:
+ * dst rows [dst_row0[i], +n_rows[i]) <- src rows [src_row0[i], +n_rows[i]).
+ * ranges: device int32 [n_ranges][3] = {dst_row0, src_row0, n_rows}.
+ * row_bytes, strides and both base pointers must be 16-byte aligned. */
+ZP_API int zp_copy_rows(void* dst, int64_t dst_stride_bytes, const void* src, int64_t src_stride_bytes,
+                 int64_t row_bytes, const int32_t* ranges, int n_ranges, int max_rows_per_range,
+                 void* stream);
+
+/* Fused remap push: for each destination d, rows [src_row0[d], +count[d]) of
+ * `src` are stored directly into peer buffer dst_ptrs[d] (a device pointer
+ * valid in this process, e.g. CUDA-IPC mapped) at row dst_row0[d].  Then the
+ * kernel release-stores `epoch` into flags_ptrs[d][my_rank] and finally waits
+ * until its own flag row (flags_ptrs[my_rank][s], s with expect[s]) reaches
+ * `epoch`.  All arrays are device int64/int32 of length world. */
+ZP_API int zp_remap_push(const void* src, int64_t row_bytes, const int64_t* dst_ptrs,
+                  const int32_t* src_row0, const int32_t* dst_row0, const int32_t* count,
+                  const int64_t* flags_ptrs, const int32_t* expect, int world, int my_rank,
+                  int32_t epoch, int max_count, void* stream);
+
+/* CUDA IPC helpers for zp_remap_push (host pointers to 64-byte handles). */
+ZP_API int zp_ipc_get_handle(void* dev_ptr, void* handle_out64);
+ZP_API int zp_ipc_open_handle(const void* handle64, void** dev_ptr_out);
+ZP_API int zp_ipc_close_handle(void* dev_ptr);
+
+/* Misc. */
+ZP_API const char* zp_last_error(void);
+ZP_API int zp_device_sm_count(void);
+ZP_API int zp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZEPPELIN_B200_H */

@@ -1,0 +1,454 @@
+// Causal varlen / ring-round flash attention forward for sm_100a.
+//
+// Executes what the reference only counts: for every query row q and every
+// key k of the same sequence with global position k <= q
+// (attention_engine.py:113-136, visible_pairs), O = softmax(q.K^T/sqrt(d)) V.
+// LocalTask work (attention_engine.py:260-265) is one launch over all local
+// fragments; each RingRound (attention_engine.py:229-244) is one launch against
+// the KV set held by the ring position (i-r) mod g, resuming the running
+// softmax state of the previous round (exact online-softmax continuation).
+//
+// CTA = one work item = 128 query rows x 2 query heads of one GQA group.
+//   warp 0      TMA producer (Q, then K/V tiles through 2-stage rings)
+//   warp 1      TMEM allocator + tcgen05.mma issuer (single thread)
+//   warps 2-3   idle (keep warpgroup 0 whole for setmaxnreg)
+//   warps 4-7   softmax / rescale / epilogue for head 2p   (thread == row)
+//   warps 8-11  softmax / rescale / epilogue for head 2p+1 (thread == row)
+// A warp may only touch TMEM lanes 32*(warp%4)..+31.  Warpgroup 0 gives its
+// registers to the two softmax warpgroups (setmaxnreg), which hold a whole
+// 128-column S row per thread.
+// TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512);
+// P_t (bf16x2 packed, 64 columns) aliases S_t columns [64,128) and feeds the
+// PV product as the TMEM A operand.  Shared memory: Q0,Q1 (2x32 KB), K and V
+// 2-stage rings (4x32 KB), all SWIZZLE_128B as written by TMA.
+#include "zp_ptx.cuh"
+#include "../../include/zeppelin_b200.h"
+
+namespace zp {
+
+constexpr int kHeadDim = 128;
+constexpr int kBM = 128;  // query rows per tile
+constexpr int kBN = 128;  // key rows per tile
+constexpr int kThreads = 384;
+constexpr uint32_t kTileBytes = kBM * kHeadDim * 2;   // 32 KB
+constexpr uint32_t kBoxBytes = 128 * 64 * 2;          // 16 KB (one 64-column TMA box)
+constexpr uint32_t kSmemQ = 0;
+constexpr uint32_t kSmemK = 2 * kTileBytes;
+constexpr uint32_t kSmemV = 4 * kTileBytes;
+constexpr uint32_t kSmemBar = 6 * kTileBytes;
+constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;  // + barriers + alignment slack
+
+// barrier slots
+enum : int {
+  B_QFULL = 0,
+  B_KFULL = 1,   // +stage
+  B_KEMPTY = 3,  // +stage
+  B_VFULL = 5,   // +stage
+  B_VEMPTY = 7,  // +stage
+  B_SFULL = 9,   // +tile
+  B_PFULL = 11,  // +tile
+  B_ODONE = 13,  // +tile
+  B_COUNT = 15
+};
+
+struct AttnArgs {
+  const zp_attn_item* items;
+  const zp_kv_seg* segs;
+  __nv_bfloat16* o;
+  float* lse;
+  float* st_o;
+  float* st_ml;
+  int lse_stride;
+  int state_rows;
+  int hq;
+  int group;  // hq / hkv
+  float scale_log2;
+};
+
+// Walks the KV tiles an item needs, in order: tiles of each segment up to the
+// item's last visible key (causal pruning; fully-masked tiles never issued).
+struct TileCursor {
+  const zp_kv_seg* segs;
+  int s, end, max_qpos, ti, nt;
+  zp_kv_seg g;
+  __device__ __forceinline__ TileCursor(const zp_kv_seg* sg, int b, int c, int mq)
+      : segs(sg), s(b - 1), end(b + c), max_qpos(mq), ti(0), nt(0) {}
+  __device__ __forceinline__ bool next() {
+    if (++ti < nt) return true;
+    while (++s < end) {
+      g = segs[s];
+      if (g.len > 0 && g.pos0 <= max_qpos) {
+        nt = (min(g.len, max_qpos - g.pos0 + 1) + kBN - 1) / kBN;
+        ti = 0;
+        return true;
+      }
+    }
+    return false;
+  }
+  __device__ __forceinline__ int row() const { return g.row0 + ti * kBN; }
+  __device__ __forceinline__ int pos() const { return g.pos0 + ti * kBN; }
+  __device__ __forceinline__ int valid() const { return min(kBN, g.len - ti * kBN); }
+};
+
+// Descriptor start addresses are in 16-byte units in the low 14 bits, so a
+// byte offset inside shared memory is added to a base descriptor as off>>4.
+__device__ __forceinline__ void issue_qk(uint32_t d_tmem, uint64_t q_desc, uint64_t k_desc,
+                                         uint32_t idesc) {
+#pragma unroll
+  for (int kk = 0; kk < kHeadDim / 16; ++kk) {
+    const uint64_t off = ((kk >> 2) * kBoxBytes + (kk & 3) * 32) >> 4;
+    mma_ss(d_tmem, q_desc + off, k_desc + off, idesc, kk > 0 ? 1u : 0u);
+  }
+}
+
+// V tile is [128 keys x 128 dims], dims contiguous: MN-major B operand.  16
+// keys per MMA = 2 groups of 8 rows (SBO 1 KB); the two 64-dim swizzle atoms
+// are one TMA box apart (LBO 16 KB).  P (A operand) is 8 TMEM columns per
+// 16 keys.
+__device__ __forceinline__ void issue_pv(uint32_t d_tmem, uint32_t p_tmem, uint64_t v_desc,
+                                         uint32_t idesc, bool accumulate) {
+#pragma unroll
+  for (int kk = 0; kk < kBN / 16; ++kk)
+    mma_ts(d_tmem, p_tmem + kk * 8, v_desc + uint64_t(kk * (2048 >> 4)), idesc,
+           (accumulate || kk > 0) ? 1u : 0u);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
+                    const __grid_constant__ CUtensorMap tm_k,
+                    const __grid_constant__ CUtensorMap tm_v, const AttnArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t sbase = (raw + 1023u) & ~1023u;
+  uint8_t* sgen = smem_raw + (sbase - raw);
+  const uint32_t bar0 = sbase + kSmemBar;
+  auto bar = [&](int i) -> uint32_t { return bar0 + 8u * uint32_t(i); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sgen + kSmemBar + 8 * B_COUNT);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const zp_attn_item it = args.items[blockIdx.x];
+  const int max_qpos = it.q_pos0 + it.q_len - 1;
+  int n_tiles = 0;
+  {
+    TileCursor cur(args.segs, it.seg_begin, it.seg_count, max_qpos);
+    while (cur.next()) ++n_tiles;
+  }
+  const bool resume = (it.flags & ZP_ITEM_LOAD_STATE) != 0;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar(B_QFULL), 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(bar(B_KFULL + s), 1);
+      mbar_init(bar(B_KEMPTY + s), 1);
+      mbar_init(bar(B_VFULL + s), 1);
+      mbar_init(bar(B_VEMPTY + s), 1);
+      mbar_init(bar(B_SFULL + s), 1);
+      mbar_init(bar(B_PFULL + s), 128);
+      mbar_init(bar(B_ODONE + s), 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(smem_u32(tmem_slot), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int kvh = (2 * it.head_pair) / args.group;
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    if (n_tiles > 0 && warp == 0 && lane == 0) {
+      // ---------------- producer: Q once, then K_j / V_j per KV tile
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      const uint64_t pol_q = policy_evict_first();
+      const uint64_t pol_kv = policy_evict_last();
+      mbar_expect_tx(bar(B_QFULL), 2 * kTileBytes);
+      for (int t = 0; t < 2; ++t)
+        for (int b = 0; b < 2; ++b)
+          tma_load_2d(sbase + kSmemQ + t * kTileBytes + b * kBoxBytes, &tm_q, bar(B_QFULL),
+                      (2 * it.head_pair + t) * kHeadDim + b * 64, it.q_row0, pol_q);
+      TileCursor cur(args.segs, it.seg_begin, it.seg_count, max_qpos);
+      for (int j = 0; cur.next(); ++j) {
+                      const int st = j & 1;
+                      const uint32_t u = uint32_t(j >> 1);
+                      const int row = cur.row();
+                      if (j >= 2) mbar_wait(bar(B_KEMPTY + st), (u - 1) & 1);
+                      mbar_expect_tx(bar(B_KFULL + st), kTileBytes);
+                      for (int b = 0; b < 2; ++b)
+                        tma_load_2d(sbase + kSmemK + st * kTileBytes + b * kBoxBytes, &tm_k,
+                                    bar(B_KFULL + st), kvh * kHeadDim + b * 64, row, pol_kv);
+                      if (j >= 2) mbar_wait(bar(B_VEMPTY + st), (u - 1) & 1);
+                      mbar_expect_tx(bar(B_VFULL + st), kTileBytes);
+                      for (int b = 0; b < 2; ++b)
+                        tma_load_2d(sbase + kSmemV + st * kTileBytes + b * kBoxBytes, &tm_v,
+                                    bar(B_VFULL + st), kvh * kHeadDim + b * 64, row, pol_kv);
+      }
+    } else if (n_tiles > 0 && warp == 1 && lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
+      constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
+      const uint32_t tS[2] = {tmem + 0, tmem + 128};
+      const uint32_t tO[2] = {tmem + 256, tmem + 384};
+      const uint64_t q_desc0 = umma_desc_sw128(sbase + kSmemQ, 16, 1024);
+      const uint64_t k_desc0 = umma_desc_sw128(sbase + kSmemK, 16, 1024);
+      const uint64_t v_desc0 = umma_desc_sw128(sbase + kSmemV, kBoxBytes, 1024);
+      const uint64_t vk_step = kTileBytes >> 4;  // one 32 KB tile, in descriptor units
+      mbar_wait(bar(B_QFULL), 0);
+      mbar_wait(bar(B_KFULL + 0), 0);
+      tc_fence_after();
+      for (int t = 0; t < 2; ++t) {
+        issue_qk(tS[t], q_desc0 + vk_step * t, k_desc0, idesc_qk);
+        tc_commit(bar(B_SFULL + t));
+      }
+      tc_commit(bar(B_KEMPTY + 0));
+      for (int j = 1; j < n_tiles; ++j) {
+        const int st = j & 1, pst = (j - 1) & 1;
+        mbar_wait(bar(B_KFULL + st), uint32_t(j >> 1) & 1);
+        mbar_wait(bar(B_VFULL + pst), uint32_t((j - 1) >> 1) & 1);
+        tc_fence_after();
+        for (int t = 0; t < 2; ++t) {
+          mbar_wait(bar(B_PFULL + t), uint32_t(j - 1) & 1);
+          tc_fence_after();
+          issue_pv(tO[t], tS[t] + 64, v_desc0 + vk_step * pst, idesc_pv, resume || (j - 1) > 0);
+          tc_commit(bar(B_ODONE + t));
+          issue_qk(tS[t], q_desc0 + vk_step * t, k_desc0 + vk_step * st, idesc_qk);
+          tc_commit(bar(B_SFULL + t));
+        }
+        tc_commit(bar(B_KEMPTY + st));
+        tc_commit(bar(B_VEMPTY + pst));
+      }
+      const int jl = n_tiles - 1, pst = jl & 1;
+      mbar_wait(bar(B_VFULL + pst), uint32_t(jl >> 1) & 1);
+      tc_fence_after();
+      for (int t = 0; t < 2; ++t) {
+        mbar_wait(bar(B_PFULL + t), uint32_t(jl) & 1);
+        tc_fence_after();
+        issue_pv(tO[t], tS[t] + 64, v_desc0 + vk_step * pst, idesc_pv, resume || jl > 0);
+        tc_commit(bar(B_ODONE + t));
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    if (n_tiles > 0) {
+      // ---------------- softmax / correction / epilogue
+      const int t = (warp - 4) >> 2;
+      const int quad = warp & 3;
+      const int row = quad * 32 + lane;
+      const uint32_t lane_bits = uint32_t(quad * 32) << 16;
+      const uint32_t tS = tmem + lane_bits + uint32_t(t * 128);
+      const uint32_t tP = tS + 64;
+      const uint32_t tO = tmem + lane_bits + 256u + uint32_t(t * 128);
+      const int h = 2 * it.head_pair + t;
+      const int qpos = it.q_pos0 + row;
+      const float sl2 = args.scale_log2;
+      float m = -INFINITY, l = 0.f;
+
+      if (resume) {
+        const int srow = it.state_row0 + row;
+        const bool ok = row < it.q_len;
+        if (ok) {
+          m = args.st_ml[size_t(h) * args.state_rows + srow];
+          l = args.st_ml[size_t(args.hq + h) * args.state_rows + srow];
+        }
+        const float4* src =
+            reinterpret_cast<const float4*>(args.st_o + (size_t(srow) * args.hq + h) * kHeadDim);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            float4 x = ok ? src[c * 8 + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+            r[4 * v + 0] = __float_as_uint(x.x);
+            r[4 * v + 1] = __float_as_uint(x.y);
+            r[4 * v + 2] = __float_as_uint(x.z);
+            r[4 * v + 3] = __float_as_uint(x.w);
+          }
+          tmem_st32(tO + c * 32, r);
+        }
+        tmem_wait_st();
+      }
+
+      TileCursor cur(args.segs, it.seg_begin, it.seg_count, max_qpos);
+      for (int j = 0; cur.next(); ++j) {
+        mbar_wait(bar(B_SFULL + t), uint32_t(j) & 1);
+        tc_fence_after();
+        float s[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tS + c * 32, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int v = 0; v < 32; ++v) s[c * 32 + v] = __uint_as_float(r[v]);
+        }
+        const int kpos0 = cur.pos();
+        const int kv_valid = cur.valid();
+        if (kv_valid < kBN || kpos0 + kBN - 1 > it.q_pos0) {
+          const int lim = min(kv_valid - 1, qpos - kpos0);  // last visible column
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (c > lim) s[c] = -INFINITY;
+        }
+        float mx = s[0];
+#pragma unroll
+        for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
+        const float m_new = fmaxf(m, mx * sl2);
+        const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
+        const float alpha = ex2(m - m_use);
+        float sum = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int v = 0; v < 16; ++v) {
+            const float p0 = ex2(fmaf(s[c * 32 + 2 * v], sl2, -m_use));
+            const float p1 = ex2(fmaf(s[c * 32 + 2 * v + 1], sl2, -m_use));
+            sum += p0 + p1;
+            pk[v] = pack_bf16(p0, p1);
+          }
+          tmem_st16(tP + c * 16, pk);
+        }
+        l = l * alpha + sum;
+        m = m_new;
+        // O_t must hold PV(j-1) before it is rescaled and before PV(j) is issued.
+        if (j > 0) {
+          mbar_wait(bar(B_ODONE + t), uint32_t(j - 1) & 1);
+          tc_fence_after();
+        }
+        if ((j > 0 || resume) && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t r[32];
+            tmem_ld32(tO + c * 32, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int v = 0; v < 32; ++v) r[v] = __float_as_uint(__uint_as_float(r[v]) * alpha);
+            tmem_st32(tO + c * 32, r);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(bar(B_PFULL + t));
+      }
+
+      // ---------------- epilogue
+      mbar_wait(bar(B_ODONE + t), uint32_t(n_tiles - 1) & 1);
+      tc_fence_after();
+      const bool ok = row < it.q_len;
+      if (it.flags & ZP_ITEM_STORE_STATE) {
+        const int srow = it.state_row0 + row;
+        float4* dst = reinterpret_cast<float4*>(args.st_o + (size_t(srow) * args.hq + h) * kHeadDim);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tO + c * 32, r);
+          tmem_wait_ld();
+          if (ok) {
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+              dst[c * 8 + v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                           __uint_as_float(r[4 * v + 2]),
+                                           __uint_as_float(r[4 * v + 3]));
+          }
+        }
+        if (ok) {
+          args.st_ml[size_t(h) * args.state_rows + srow] = m;
+          args.st_ml[size_t(args.hq + h) * args.state_rows + srow] = l;
+        }
+      } else {
+        const float inv_l = l > 0.f ? 1.f / l : 0.f;
+        uint4* dst = reinterpret_cast<uint4*>(args.o + (size_t(it.q_row0 + row) * args.hq + h) *
+                                                           kHeadDim);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tO + c * 32, r);
+          tmem_wait_ld();
+          if (ok) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint4 w;
+              w.x = pack_bf16(__uint_as_float(r[8 * v + 0]) * inv_l, __uint_as_float(r[8 * v + 1]) * inv_l);
+              w.y = pack_bf16(__uint_as_float(r[8 * v + 2]) * inv_l, __uint_as_float(r[8 * v + 3]) * inv_l);
+              w.z = pack_bf16(__uint_as_float(r[8 * v + 4]) * inv_l, __uint_as_float(r[8 * v + 5]) * inv_l);
+              w.w = pack_bf16(__uint_as_float(r[8 * v + 6]) * inv_l, __uint_as_float(r[8 * v + 7]) * inv_l);
+              dst[c * 4 + v] = w;
+            }
+          }
+        }
+        if (ok) {
+          const float lse = l > 0.f ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
+          args.lse[size_t(h) * args.lse_stride + it.q_row0 + row] = lse;
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+}  // namespace zp
+
+// ------------------------------------------------------------------ host side
+#include "zp_host.h"
+
+extern "C" int zp_attn_fwd(const void* q, const void* k, const void* v, int q_rows, int kv_rows,
+                           int kv_row_stride, int hq, int hkv, int head_dim, void* o, float* lse,
+                           int lse_stride, const zp_attn_item* items, int n_items,
+                           const zp_kv_seg* segs, float* state_o, float* state_ml,
+                           int state_rows, float softmax_scale, void* stream) {
+  using namespace zp;
+  if (head_dim != kHeadDim) return zp_fail(ZP_EINVAL, "zp_attn_fwd: head_dim must be 128");
+  if (hq <= 0 || hkv <= 0 || hq % hkv != 0 || (hq / hkv) % 2 != 0)
+    return zp_fail(ZP_EINVAL, "zp_attn_fwd: need hq % hkv == 0 and an even GQA group size");
+  if (n_items < 0 || q_rows < 0 || kv_rows < 0 || kv_row_stride < hkv * kHeadDim)
+    return zp_fail(ZP_EINVAL, "zp_attn_fwd: bad sizes");
+  if (n_items == 0) return ZP_OK;
+  if (q_rows == 0 || kv_rows == 0) return zp_fail(ZP_EINVAL, "zp_attn_fwd: empty q or kv with items");
+  if (!q || !k || !v || !o || !lse || !items || !segs)
+    return zp_fail(ZP_EINVAL, "zp_attn_fwd: null pointer");
+  if (zp_check_device() != ZP_OK) return ZP_ENODEV;
+
+  CUtensorMap tq, tk, tv;
+  int rc;
+  if ((rc = zp_make_tmap_2d_bf16(&tq, q, uint64_t(hq) * kHeadDim, uint64_t(q_rows),
+                                 uint64_t(hq) * kHeadDim * 2, 64, 128)) != ZP_OK)
+    return rc;
+  if ((rc = zp_make_tmap_2d_bf16(&tk, k, uint64_t(hkv) * kHeadDim, uint64_t(kv_rows),
+                                 uint64_t(kv_row_stride) * 2, 64, 128)) != ZP_OK)
+    return rc;
+  if ((rc = zp_make_tmap_2d_bf16(&tv, v, uint64_t(hkv) * kHeadDim, uint64_t(kv_rows),
+                                 uint64_t(kv_row_stride) * 2, 64, 128)) != ZP_OK)
+    return rc;
+
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kSmemBytes));
+    if (e != cudaSuccess) return zp_fail_cuda(e, "zp_attn_fwd: smem attribute");
+    attr_done = true;
+  }
+  AttnArgs a;
+  a.items = items;
+  a.segs = segs;
+  a.o = reinterpret_cast<__nv_bfloat16*>(o);
+  a.lse = lse;
+  a.st_o = state_o;
+  a.st_ml = state_ml;
+  a.lse_stride = lse_stride;
+  a.state_rows = state_rows;
+  a.hq = hq;
+  a.group = hq / hkv;
+  a.scale_log2 = softmax_scale * 1.4426950408889634f;
+  attn_fwd_kernel<<<n_items, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(
+      tq, tk, tv, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_attn_fwd: launch");
+  return ZP_OK;
+}

@@ -1,0 +1,104 @@
+"""Device entry points over the C ABI, taking torch tensors.
+
+torch is used only for device memory and streams; every byte of attention or
+remap data is produced by the sm_100a kernels in ``csrc/``.  Nothing here has a
+CPU path: inputs must be CUDA tensors and the library must load.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _native
+from .worklist import QueryFragment, WorkList, build_worklist
+
+HEAD_DIM = 128
+
+
+def _stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _require_cuda(*tensors: torch.Tensor) -> None:
+    for t in tensors:
+        if not t.is_cuda:
+            raise RuntimeError("zeppelin-b200 ops run on CUDA tensors only (no CPU fallback)")
+
+
+def upload_worklist(wl: WorkList, device: torch.device) -> tuple[torch.Tensor, torch.Tensor]:
+    """Copy the item / segment tables to the device (one H2D each)."""
+    items = torch.from_numpy(wl.items.view(np.int32).reshape(-1)).pin_memory().to(device, non_blocking=True)
+    segs = torch.from_numpy(wl.segs.view(np.int32).reshape(-1)).pin_memory().to(device, non_blocking=True)
+    return items, segs
+
+
+def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, items: torch.Tensor, n_items: int,
+             segs: torch.Tensor, o: torch.Tensor, lse: torch.Tensor,
+             state_o: torch.Tensor | None = None, state_ml: torch.Tensor | None = None,
+             softmax_scale: float | None = None, stream: torch.cuda.Stream | None = None) -> None:
+    """Launch zp_attn_fwd over a device work list.
+
+    q: [Tq, Hq, 128] bf16, k/v: [Tk, Hkv, 128] bf16 views whose row stride may
+    exceed Hkv*128 (interleaved ring buffers), o: [Tq, Hq, 128] bf16,
+    lse: [Hq, Tq] fp32."""
+    _require_cuda(q, k, v, o, lse)
+    tq, hq, d = q.shape
+    tk, hkv, dk = k.shape
+    if d != HEAD_DIM or dk != HEAD_DIM or v.shape != k.shape:
+        raise ValueError("head_dim must be 128 and k/v must have equal shapes")
+    if q.dtype != torch.bfloat16 or k.dtype != torch.bfloat16 or v.dtype != torch.bfloat16:
+        raise ValueError("q/k/v must be bf16")
+    if q.stride() != (hq * d, d, 1) or o.stride() != (hq * d, d, 1):
+        raise ValueError("q and o must be row-contiguous [T, H, 128]")
+    if k.stride()[1:] != (d, 1) or v.stride() != k.stride():
+        raise ValueError("k/v must have contiguous heads and equal strides")
+    if lse.dtype != torch.float32 or lse.shape[0] != hq:
+        raise ValueError("lse must be fp32 [Hq, >=Tq]")
+    scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
+    st_o = state_o.data_ptr() if state_o is not None else None
+    st_ml = state_ml.data_ptr() if state_ml is not None else None
+    st_rows = int(state_o.shape[0]) if state_o is not None else 0
+    _native.call("zp_attn_fwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), tq, tk, k.stride(0),
+                 hq, hkv, d, o.data_ptr(), lse.data_ptr(), lse.stride(0), items.data_ptr(),
+                 n_items, segs.data_ptr(), st_o, st_ml, st_rows, scale, _stream_ptr(stream))
+
+
+def local_fragments(seqlens: list[int] | np.ndarray, row0: int = 0) -> list[QueryFragment]:
+    """Whole-sequence causal fragments for sequences packed back to back."""
+    frags = []
+    r = row0
+    for n in seqlens:
+        n = int(n)
+        frags.append(QueryFragment(row0=r, pos0=0, length=n, segs=[(r, 0, n)]))
+        r += n
+    return frags
+
+
+def varlen_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seqlens,
+                     softmax_scale: float | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Causal attention of packed variable-length sequences (all GPU-local):
+    the LocalTask queue of one rank.  Returns (o bf16 [T,Hq,128], lse fp32 [Hq,T])."""
+    _require_cuda(q, k, v)
+    t, hq, _ = q.shape
+    hkv = k.shape[1]
+    wl = build_worklist(local_fragments(seqlens), hq // 2)
+    o = torch.empty_like(q)
+    lse = torch.empty(hq, t, dtype=torch.float32, device=q.device)
+    items, segs = upload_worklist(wl, q.device)
+    attn_fwd(q, k, v, items, wl.n_items, segs, o, lse, softmax_scale=softmax_scale)
+    return o, lse
+
+
+def copy_rows(dst: torch.Tensor, src: torch.Tensor, ranges: torch.Tensor, n_ranges: int,
+              max_rows: int, stream: torch.cuda.Stream | None = None) -> None:
+    """dst[d0:d0+n] = src[s0:s0+n] for each (d0, s0, n) row of the int32
+    device table ``ranges``; rows are the leading dimension of both tensors."""
+    _require_cuda(dst, src, ranges)
+    row_bytes = src[0].numel() * src.element_size() if src.shape[0] else dst[0].numel() * dst.element_size()
+    _native.call("zp_copy_rows", dst.data_ptr(), dst.stride(0) * dst.element_size(), src.data_ptr(),
+                 src.stride(0) * src.element_size(), row_bytes, ranges.data_ptr(), n_ranges,
+                 max_rows, _stream_ptr(stream))

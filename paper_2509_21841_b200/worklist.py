@@ -1,0 +1,140 @@
+"""Host-side work lists for the attention kernel (``zp_attn_fwd``).
+
+A work item is one 128-row query tile of one sequence fragment for one pair
+of query heads sharing a KV head.  Items carry the KV segments they attend to
+(global in-sequence positions), so the same kernel executes
+
+* LocalTask work: a whole sequence against itself
+  (reference ``attention_engine.py:260-265``), and
+* one RingRound: a position's query ranges against the KV ranges held by ring
+  position ``(i - r) mod g`` (reference ``attention_engine.py:229-244``),
+
+with the causal rule of ``visible_pairs`` (``attention_engine.py:113-136``):
+key position <= query position.  Items are sorted longest-first (LPT) so the
+hardware block scheduler drains the long causal tiles early.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+TILE = 128
+ITEM_LOAD_STATE = 1
+ITEM_STORE_STATE = 2
+
+ITEM_DTYPE = np.dtype([("q_row0", "<i4"), ("q_pos0", "<i4"), ("q_len", "<i4"),
+                       ("head_pair", "<i4"), ("seg_begin", "<i4"), ("seg_count", "<i4"),
+                       ("state_row0", "<i4"), ("flags", "<i4")])
+SEG_DTYPE = np.dtype([("row0", "<i4"), ("pos0", "<i4"), ("len", "<i4"), ("reserved", "<i4")])
+
+
+@dataclass
+class QueryFragment:
+    """Query rows [row0, row0+length) holding global positions [pos0, ...),
+    attending to KV segments ``segs`` = [(row0, pos0, len), ...] of the same
+    sequence.  ``state_row0`` locates the fragment in ring partial-state
+    buffers (-1 when unused)."""
+
+    row0: int
+    pos0: int
+    length: int
+    segs: list[tuple[int, int, int]]
+    state_row0: int = -1
+
+
+def kv_tile_counts(max_qpos: np.ndarray, segs: list[tuple[int, int, int]]) -> np.ndarray:
+    """Number of 128-key tiles the kernel walks for query tiles whose last
+    position is ``max_qpos`` (matches TileCursor in zp_attn.cu)."""
+    n = np.zeros_like(max_qpos, dtype=np.int64)
+    for _, p0, ln in segs:
+        if ln <= 0:
+            continue
+        vis = np.minimum(ln, max_qpos - p0 + 1)
+        n += np.where(max_qpos >= p0, (vis + TILE - 1) // TILE, 0)
+    return n
+
+
+def tile_visible_pairs(q_pos0: np.ndarray, q_len: np.ndarray, segs: list[tuple[int, int, int]]) -> np.ndarray:
+    """Exact visible (q,k) pairs per query tile (closed form of visible_pairs,
+    reference attention_engine.py:113-136, vectorised over tiles)."""
+    a = q_pos0.astype(np.int64)
+    b = a + q_len.astype(np.int64)
+    total = np.zeros_like(a)
+    for _, c, m in segs:
+        if m <= 0:
+            continue
+        d = c + m
+        lo = np.maximum(a, c)
+        hi = np.minimum(b - 1, d - 2)
+        cnt = np.maximum(hi - lo + 1, 0)
+        total += np.where(cnt > 0, ((lo + 1 - c) + (hi + 1 - c)) * cnt // 2, 0)
+        flat_lo = np.maximum(a, d - 1)
+        total += np.maximum(b - flat_lo, 0) * m
+    return total
+
+
+@dataclass
+class WorkList:
+    items: np.ndarray      # ITEM_DTYPE, sorted longest-first
+    segs: np.ndarray       # SEG_DTYPE
+    pairs_per_head: int    # visible causal pairs for one query head
+    kv_tiles: int          # sum over items of KV tiles walked
+
+    @property
+    def n_items(self) -> int:
+        return int(self.items.shape[0])
+
+
+def build_worklist(frags: list[QueryFragment], n_head_pairs: int,
+                   tile_flags=None) -> WorkList:
+    """Expand fragments into 128-row tiles x head pairs.
+
+    ``tile_flags(frag_index, tile_q_pos0, tile_len) -> int array`` may attach
+    ZP_ITEM_* flags per tile (ring rounds); tiles with no visible pair are
+    dropped (they would be pure no-ops)."""
+    seg_rows: list[tuple[int, int, int, int]] = []
+    cols = {name: [] for name in ("q_row0", "q_pos0", "q_len", "seg_begin", "seg_count",
+                                  "state_row0", "flags", "cost")}
+    pairs = 0
+    for fi, f in enumerate(frags):
+        if f.length <= 0:
+            continue
+        seg_begin = len(seg_rows)
+        seg_rows.extend((r, p, n, 0) for r, p, n in f.segs)
+        offs = np.arange(0, f.length, TILE, dtype=np.int64)
+        q_len = np.minimum(TILE, f.length - offs)
+        q_pos0 = f.pos0 + offs
+        cost = kv_tile_counts(q_pos0 + q_len - 1, f.segs)
+        vis = tile_visible_pairs(q_pos0, q_len, f.segs)
+        keep = vis > 0
+        if not keep.any():
+            continue
+        flags = np.zeros_like(offs) if tile_flags is None else np.asarray(tile_flags(fi, q_pos0, q_len))
+        pairs += int(vis[keep].sum())
+        k = int(keep.sum())
+        cols["q_row0"].append(f.row0 + offs[keep])
+        cols["q_pos0"].append(q_pos0[keep])
+        cols["q_len"].append(q_len[keep])
+        cols["seg_begin"].append(np.full(k, seg_begin))
+        cols["seg_count"].append(np.full(k, len(f.segs)))
+        cols["state_row0"].append((f.state_row0 + offs[keep]) if f.state_row0 >= 0 else np.full(k, -1))
+        cols["flags"].append(flags[keep])
+        cols["cost"].append(cost[keep])
+    segs = np.zeros(max(len(seg_rows), 1), dtype=SEG_DTYPE)
+    for i, row in enumerate(seg_rows):
+        segs[i] = row
+    if not cols["q_row0"]:
+        return WorkList(np.zeros(0, dtype=ITEM_DTYPE), segs, 0, 0)
+    tiles = {k: np.concatenate(v) for k, v in cols.items()}
+    n_tiles = tiles["q_row0"].shape[0]
+    # longest tiles first; the head pairs of one tile stay adjacent so CTAs
+    # running together share K/V tiles in L2.
+    order = np.argsort(-tiles["cost"], kind="stable")
+    items = np.zeros(n_tiles * n_head_pairs, dtype=ITEM_DTYPE)
+    for name in ("q_row0", "q_pos0", "q_len", "seg_begin", "seg_count", "state_row0", "flags"):
+        items[name] = np.repeat(tiles[name][order], n_head_pairs)
+    items["head_pair"] = np.tile(np.arange(n_head_pairs), n_tiles)
+    kv_tiles = int(tiles["cost"].sum()) * n_head_pairs
+    return WorkList(items, segs, pairs, kv_tiles)

@@ -1,0 +1,87 @@
+"""K1 (local varlen causal attention) and ring-resume parity on a B200.
+
+Reference for this floating-point kernel: plain PyTorch fp32 attention on the
+same bf16-rounded inputs (per sequence, GQA expanded), tolerance max-abs 2e-2
+on the bf16 output (BASELINE.json north_star)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2509_21841_b200 import ops
+from paper_2509_21841_b200.worklist import QueryFragment, build_worklist, ITEM_LOAD_STATE, ITEM_STORE_STATE
+
+MAX_ABS = 2e-2
+
+
+def ref_attention(q, k, v, qpos, kpos):
+    """fp32 reference: q [n,H,d], k/v [m,Hkv,d], mask kpos <= qpos."""
+    hq, hkv = q.shape[1], k.shape[1]
+    qf = q.float().transpose(0, 1)
+    kf = k.float().repeat_interleave(hq // hkv, dim=1).transpose(0, 1)
+    vf = v.float().repeat_interleave(hq // hkv, dim=1).transpose(0, 1)
+    s = torch.matmul(qf, kf.transpose(1, 2)) / math.sqrt(q.shape[-1])
+    mask = kpos[None, :] <= qpos[:, None]
+    s = s.masked_fill(~mask[None], float("-inf"))
+    lse = torch.logsumexp(s, dim=-1)
+    o = torch.matmul(torch.softmax(s, dim=-1), vf).transpose(0, 1)
+    return o, lse
+
+
+def make_qkv(t, hq=32, hkv=8, seed=0):
+    g = torch.Generator().manual_seed(seed)
+    q = torch.randn(t, hq, 128, generator=g).to(torch.bfloat16).cuda()
+    k = torch.randn(t, hkv, 128, generator=g).to(torch.bfloat16).cuda()
+    v = torch.randn(t, hkv, 128, generator=g).to(torch.bfloat16).cuda()
+    return q, k, v
+
+
+@pytest.mark.parametrize("seqlens", [[128], [1], [77], [300, 5, 129, 1000], [2048, 17, 640]])
+def test_varlen_local_matches_fp32(seqlens):
+    t = sum(seqlens)
+    q, k, v = make_qkv(t, seed=len(seqlens))
+    o, lse = ops.varlen_attention(q, k, v, seqlens)
+    torch.cuda.synchronize()
+    r = 0
+    for n in seqlens:
+        pos = torch.arange(n, device="cuda")
+        ro, rl = ref_attention(q[r:r + n], k[r:r + n], v[r:r + n], pos, pos)
+        err = (o[r:r + n].float() - ro).abs().max().item()
+        assert err <= MAX_ABS, (n, err)
+        lerr = (lse[:, r:r + n] - rl).abs().max().item()
+        assert lerr <= 1e-2, (n, lerr)
+        r += n
+
+
+def test_resume_state_equals_single_pass():
+    """Two launches over two KV segments (ring-round style, with partial
+    state) equal one launch over both segments."""
+    n = 700
+    q, k, v = make_qkv(n, seed=3)
+    hq = q.shape[1]
+    full = build_worklist([QueryFragment(0, 0, n, [(0, 0, n)])], hq // 2)
+    o1 = torch.empty_like(q)
+    l1 = torch.empty(hq, n, device="cuda")
+    it, sg = ops.upload_worklist(full, q.device)
+    ops.attn_fwd(q, k, v, it, full.n_items, sg, o1, l1)
+    # split keys [0,300) + [300,700); the second launch resumes
+    st_o = torch.zeros(n, hq, 128, device="cuda")
+    st_ml = torch.zeros(2, hq, n, device="cuda")
+    o2 = torch.empty_like(q)
+    l2 = torch.empty(hq, n, device="cuda")
+    a = build_worklist([QueryFragment(0, 0, n, [(0, 0, 300)], state_row0=0)], hq // 2,
+                       tile_flags=lambda fi, p0, ln: np.full(p0.shape, ITEM_STORE_STATE))
+    b = build_worklist([QueryFragment(0, 0, n, [(300, 300, 400)], state_row0=0)], hq // 2,
+                       tile_flags=lambda fi, p0, ln: np.full(p0.shape, ITEM_LOAD_STATE))
+    it, sg = ops.upload_worklist(a, q.device)
+    ops.attn_fwd(q, k, v, it, a.n_items, sg, o2, l2, st_o, st_ml)
+    it, sg = ops.upload_worklist(b, q.device)
+    ops.attn_fwd(q, k, v, it, b.n_items, sg, o2, l2, st_o, st_ml)
+    torch.cuda.synchronize()
+    # tiles entirely before key 300 never see segment b (only partials stored)
+    rows = slice(256, n)
+    assert (o1[rows].float() - o2[rows].float()).abs().max().item() <= 1e-2
+    assert (l1[:, rows] - l2[:, rows]).abs().max().item() <= 1e-3
