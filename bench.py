@@ -1,0 +1,437 @@
+#!/usr/bin/env python
+"""Benchmark of the Zeppelin per-layer hot path on B200s (BASELINE.json metric).
+
+A step = one pass of the hot path over one synthetic batch: host planner
+(build_plan + build_schedule + solve_remap + per-rank work lists) -> attention
+engine (local varlen kernel + ring rounds over NVLink) -> remap to the linear
+layout -> inverse remap.  Prints ONE JSON line on rank 0.
+
+  N = 1: config 2 — Llama-3-8B attention layer (32 Q / 8 KV heads, d128, bf16)
+         on a 64K-token github-mixture batch (seed 0), all sequences local.
+  N > 1: config 3 — weak scaling, 64K tokens per GPU, one 128K sequence plus a
+         github<=128K sample (seed 1), split across GPUs by the planner; ring
+         KV exchange over NVLink + remap all-to-allv.
+
+  --impl reference: the reference's CPU path (the oracle port: numpy fp32
+  attention + remap on the planner's plan) on the host cores, bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "attn+remap layer tokens/s at 1/2/4/8 B200; % of tensor/NVLink roofline"
+UNIT = "tokens/s"
+FLOP_PER_PAIR = 4 * 128 * 32  # QK^T + PV, forward, d=128, Hq=32
+HIDDEN_BYTES = 4096 * 2        # remap row: hidden 4096 bf16
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["bf16_tflops"], p.get("bf16_tflops_sustained"), p["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def workload(n_gpus: int):
+    from paper_2509_21841_b200 import workloads as W
+    if n_gpus == 1:
+        batch = W.c2_batch("github", 0)
+        name = "C2: Llama-3-8B attention layer, 64K-token github batch (seed 0), all local, 1 B200"
+    else:
+        batch = W.c3_batch(n_gpus)
+        name = (f"C3: Llama-3-8B attention+remap layer, {65536 * n_gpus}-token long-context mixture "
+                f"(128K seq + github<=128K, seed 1), {n_gpus} B200 ring/NVLink")
+    return name, batch, W.cluster_for(batch, n_gpus)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- GPU arm
+
+def run_gpu(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_21841_b200 import engine, ops
+    from paper_2509_21841_b200 import plan as P, remap as M, schedule as S
+    from paper_2509_21841_b200.program import build_rank_program
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    ctx = engine.RankContext(rank, world, dev)
+    name, batch, cluster = workload(world)
+    hq, hkv, d = 32, 8, 128
+
+    def host_plan():
+        plan = P.build_plan(batch, cluster)
+        sched = S.build_schedule(plan)
+        res = M.solve_remap(plan.tokens_per_rank, M.cost_matrix(cluster))
+        prog = build_rank_program(plan, sched, rank, hq, res)
+        return plan, sched, prog, engine.DeviceProgram(prog, dev)
+
+    plan, sched, prog, devp = host_plan()
+    rows = prog.rows
+    lay = prog.remap
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    q = torch.randn(rows, hq, d, device=dev, generator=g, dtype=torch.bfloat16)
+    k = torch.randn(rows, hkv, d, device=dev, generator=g, dtype=torch.bfloat16)
+    v = torch.randn(rows, hkv, d, device=dev, generator=g, dtype=torch.bfloat16)
+    # one activation buffer with max(A_r, B_r) rows: the attention layout is
+    # its prefix [0, A_r), the linear layout its prefix [0, B_r); kept rows
+    # never move, only the remapped tail crosses NVLink.
+    lin_rows = max(lay.linear_rows[rank], rows, 1)
+    act = torch.empty(lin_rows, hq * d, device=dev, dtype=torch.bfloat16)
+    o = act[:rows].view(rows, hq, d)
+    lse = torch.empty(hq, max(rows, 1), device=dev)
+
+    attn_events: list[tuple] = []
+
+    def step(record=False):
+        plan_, sched_, prog_, devp_ = host_plan()
+        if record:
+            ops.set_launch_hook(lambda name, a, b: attn_events.append((name, a, b)))
+        engine.attention_forward(plan_, sched_, q, k, v, ctx, prog_, devp_, out=(o, lse))
+        ops.set_launch_hook(None)
+        yy = engine.remap_forward(prog_.remap, act[:rows], ctx, out=act[:prog_.remap.linear_rows[rank]])
+        engine.remap_inverse(prog_.remap, yy, ctx, out=act[:rows])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ops.reset_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0.record()
+        for _ in range(args.steps):
+            step(record=True)
+        e1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = ops.launch_count()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms_local], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    total_tokens = batch.total_tokens
+    value = total_tokens / (ms / 1e3)
+
+    # dominant kernel: attention launches on this rank inside the timed region
+    attn_ms = sum(a.elapsed_time(b) for _, a, b in attn_events) / args.steps
+    rank_pairs = prog.pairs_per_head()
+    rank_flop = rank_pairs * FLOP_PER_PAIR
+    peak, peak_sus, hbm, peak_kind = _peaks()
+    achieved = rank_flop / (attn_ms / 1e3) / 1e12 if attn_ms > 0 else 0.0
+    stats = torch.tensor([achieved, attn_ms, float(rank_pairs), float(len(attn_events) / args.steps)],
+                         device=dev, dtype=torch.float64)
+    if world > 1:
+        gathered = [torch.zeros_like(stats) for _ in range(world)]
+        dist.all_gather(gathered, stats)
+    else:
+        gathered = [stats]
+    per_rank = [x.tolist() for x in gathered]
+    busiest = max(range(world), key=lambda i: per_rank[i][2])
+    moved = lay.moved_rows()
+
+    # end to end through the public API with host buffers (pinned), rank-local
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, ctx, dev, rows, hq, hkv, d, host_plan, world, rank)
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    traffic = None
+    prof_path = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    if os.path.exists(prof_path):
+        try:
+            traffic = json.load(open(prof_path)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (seeded batch from the reference's length mixtures; N(0,1) q/k/v)",
+        "config": {
+            "workload": name,
+            "total_tokens": total_tokens,
+            "sequences": len(batch),
+            "heads": [hq, hkv, d],
+            "rings": len(plan.ring_groups),
+            "remap_rows_moved": moved,
+            "l2": "inputs larger than L2 (q/k/v %.0f MB per GPU > 126 MB)" % (rows * (hq + 2 * hkv) * d * 2 / 1e6),
+            "parallelism": f"zeppelin plan over {world} GPU(s), one process per GPU",
+        },
+        "roofline": {
+            "bound": "tensor",
+            "achieved": achieved if world == 1 else per_rank[busiest][0],
+            "peak": peak,
+            "unit": "TFLOP/s",
+            "frac": (achieved if world == 1 else per_rank[busiest][0]) / peak,
+            "frac_of_sustained": ((achieved if world == 1 else per_rank[busiest][0]) / peak_sus) if peak_sus else None,
+            "peak_kind": f"{peak_kind} burst bf16 (MEASURED_PEAKS.json)",
+            "traffic": traffic,
+            "kernel": "zp_attn_fwd (attn_fwd_kernel)",
+            "flop_per_pair": FLOP_PER_PAIR,
+            "rank": busiest,
+            "rank_pairs": int(per_rank[busiest][2]),
+            "attn_ms_per_step": per_rank[busiest][1],
+            "aggregate_tflops": sum(r[2] for r in per_rank) * FLOP_PER_PAIR / (ms / 1e3) / 1e12,
+        },
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(plan, sched, args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, ctx, dev, rows, hq, hkv, d, host_plan, world, rank):
+    """Same metric through the public API with pinned host inputs: every step
+    copies q/k/v H2D and reads the attention output O back D2H."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_21841_b200 import engine
+
+    hq_d = hq * d
+    hq_ = torch.randn(rows, hq, d, dtype=torch.bfloat16).pin_memory()
+    hk_ = torch.randn(rows, hkv, d, dtype=torch.bfloat16).pin_memory()
+    hv_ = torch.randn(rows, hkv, d, dtype=torch.bfloat16).pin_memory()
+    ho_ = torch.empty(rows, hq, d, dtype=torch.bfloat16).pin_memory()
+
+    def one():
+        plan_, sched_, prog_, devp_ = host_plan()
+        q = hq_.to(dev, non_blocking=True)
+        k = hk_.to(dev, non_blocking=True)
+        v = hv_.to(dev, non_blocking=True)
+        b_rows = prog_.remap.linear_rows[rank]
+        act = torch.empty(max(rows, b_rows, 1), hq_d, device=dev, dtype=torch.bfloat16)
+        lse = torch.empty(hq, max(rows, 1), device=dev)
+        engine.attention_forward(plan_, sched_, q, k, v, ctx, prog_, devp_, out=(act[:rows].view(rows, hq, d), lse))
+        y = engine.remap_forward(prog_.remap, act[:rows], ctx, out=act[:b_rows])
+        x = engine.remap_inverse(prog_.remap, y, ctx, out=act[:rows])
+        ho_.view(rows, hq_d).copy_(x, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        one()
+    e1.record()
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) * 1e3 / args.steps
+    ms = max(e0.elapsed_time(e1) / args.steps, wall)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    _, batch, _ = workload(world)
+    return {"value": batch.total_tokens / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+            "h2d_bytes_per_step": int((hq_.numel() + hk_.numel() + hv_.numel()) * 2),
+            "d2h_bytes_per_step": int(ho_.numel() * 2),
+            "api": "paper_2509_21841_b200.engine.attention_forward + remap_forward + remap_inverse"}
+
+
+# ---------------------------------------------------------------------------- CPU arm
+
+def cpu_baseline(plan, sched, seconds: float):
+    """The oracle port (numpy fp32 attention; threads = all host cores) on a
+    bounded sample of the step's attention work, extrapolated by exact pairs."""
+    import numpy as np
+
+    from oracle import attention as OA
+
+    cores = os.cpu_count() or 1
+    rng = np.random.default_rng(0)
+    sizes = sorted(plan.sequence_lengths.items(), key=lambda kv: -kv[1])
+    total_pairs = sum(n * (n + 1) // 2 for _, n in sizes)
+    # sample: query rows of the longest sequence, growing until the time budget
+    sid, n = sizes[0]
+    hq, hkv, d = 32, 8, 128
+    k = rng.standard_normal((n, hkv, d), dtype=np.float32)
+    v = rng.standard_normal((n, hkv, d), dtype=np.float32)
+    done_pairs, spent, rows = 0, 0.0, 0
+    block = 256
+    while spent < seconds and rows < n:
+        r1 = min(n, rows + block)
+        q = rng.standard_normal((r1 - rows, hq, d), dtype=np.float32)
+        t0 = time.perf_counter()
+        _, _, pairs = OA.causal_attention(q, k[:r1], v[:r1], np.arange(rows, r1), np.arange(r1), d ** -0.5,
+                                          dtype=np.float32)
+        spent += time.perf_counter() - t0
+        done_pairs += pairs
+        rows = r1
+        block = min(block * 2, 4096)
+    est = spent * total_pairs / max(done_pairs, 1)
+    total_tokens = sum(x for _, x in sizes)
+    return {"value": total_tokens / est, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"oracle numpy fp32 causal attention, query rows [0,{rows}) of the {n}-token sequence "
+                      f"({done_pairs} of {total_pairs} pairs, {spent:.1f} s), extrapolated by exact pair count; "
+                      f"remap is a no-op at N=1 and the planner (<1 ms) is excluded"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle import remap as OR
+    from paper_2509_21841_b200 import plan as P, remap as M, schedule as S
+
+    name, batch, cluster = workload(args.gpus)
+    plan = P.build_plan(batch, cluster)
+    sched = S.build_schedule(plan)
+    per_step = max(5.0, min(30.0, 150.0 / max(1, args.steps + args.warmup)))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(plan, sched, per_step)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+    # the remap's CPU cost (numpy row moves) is added for N > 1
+    remap_note = ""
+    if args.gpus > 1:
+        lay = M.remap_layout(plan.tokens_per_rank)
+        xs = [np.zeros((n, 4096), dtype=np.float16) for n in plan.tokens_per_rank]
+        t0 = time.perf_counter()
+        y = OR.forward(xs, lay.matrix)
+        OR.inverse(y, lay.matrix, list(plan.tokens_per_rank))
+        remap_s = time.perf_counter() - t0
+        vals = [batch.total_tokens / (batch.total_tokens / v + remap_s) for v in vals]
+        remap_note = f"; + numpy remap fwd/inv of all ranks ({remap_s * 1e3:.0f} ms)"
+    value = statistics.median(vals)
+    ms = batch.total_tokens / value * 1e3
+    print(json.dumps({
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+        "config": {"workload": name, "total_tokens": batch.total_tokens},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb["cores"], "kind": "port",
+                         "sample": cb["sample"] + remap_note},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["zeppelin", "reference"], default="zeppelin")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "zeppelin":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,65 @@
+"""CPU interpreter of the kernel's work-item contract (zp_attn_item / zp_kv_seg,
+include/zeppelin_b200.h) — test infrastructure.
+
+It executes a work list exactly as documented for ``zp_attn_fwd`` (tile of
+<=128 query rows x head pair, KV segments with global positions, causal mask
+k_pos <= q_pos, partial-state load/store flags), in float64, so host-side
+tables can be validated against ``attention.run_plan`` on a CPU and the GPU
+kernel can be validated against the same tables.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+LOAD, STORE = 1, 2
+
+
+class State:
+    def __init__(self, rows, hq, d):
+        self.o = np.zeros((rows, hq, d))
+        self.m = np.full((hq, rows), -np.inf)
+        self.l = np.zeros((hq, rows))
+
+
+def run_items(items, segs, q, k, v, o, lse, state, scale):
+    """q [Tq,Hq,d], k/v [Tk,Hkv,d] (float64 arrays); o/lse written in place."""
+    hq = q.shape[1]
+    grp = hq // k.shape[1]
+    for it in items:
+        r0, p0, n = int(it["q_row0"]), int(it["q_pos0"]), int(it["q_len"])
+        qpos = p0 + np.arange(n)
+        kr, kp = [], []
+        for s in segs[int(it["seg_begin"]): int(it["seg_begin"]) + int(it["seg_count"])]:
+            kr.append(int(s["row0"]) + np.arange(int(s["len"])))
+            kp.append(int(s["pos0"]) + np.arange(int(s["len"])))
+        kr = np.concatenate(kr)
+        kp = np.concatenate(kp)
+        vis = kp[None, :] <= qpos[:, None]
+        for h in (2 * int(it["head_pair"]), 2 * int(it["head_pair"]) + 1):
+            sc = q[r0:r0 + n, h, :] @ k[kr, h // grp, :].T * scale
+            sc = np.where(vis, sc, -np.inf)
+            if it["flags"] & LOAD:
+                s0 = int(it["state_row0"])
+                m_old = state.m[h, s0:s0 + n]
+                l_old = state.l[h, s0:s0 + n]
+                o_old = state.o[s0:s0 + n, h, :]
+            else:
+                m_old = np.full(n, -np.inf)
+                l_old = np.zeros(n)
+                o_old = np.zeros((n, q.shape[2]))
+            m_new = np.maximum(m_old, sc.max(axis=1))
+            m_use = np.where(np.isfinite(m_new), m_new, 0.0)
+            alpha = np.exp(m_old - m_use)
+            p = np.exp(sc - m_use[:, None])
+            l_new = l_old * alpha + p.sum(axis=1)
+            o_new = o_old * alpha[:, None] + p @ v[kr, h // grp, :]
+            if it["flags"] & STORE:
+                s0 = int(it["state_row0"])
+                state.m[h, s0:s0 + n] = m_new
+                state.l[h, s0:s0 + n] = l_new
+                state.o[s0:s0 + n, h, :] = o_new
+            else:
+                with np.errstate(invalid="ignore", divide="ignore"):
+                    o[r0:r0 + n, h, :] = np.where(l_new[:, None] > 0, o_new / l_new[:, None], 0.0)
+                    lse[h, r0:r0 + n] = np.where(l_new > 0, m_use + np.log(l_new), -np.inf)

@@ -1,0 +1,282 @@
+"""Device executor: runs a rank's program (``program.py``) on its B200.
+
+One process per GPU.  Compute goes to the caller's current CUDA stream; ring
+KV exchange goes to a dedicated communication stream (NCCL point-to-point via
+``torch.distributed``), double-buffered so round r's attention overlaps the
+transfer of round r+1's KV set.  Rings run in ``schedule.rings()`` order on
+every rank, so rings that share ranks are entered in the same order
+everywhere (deadlock-free); a rank never waits on a ring it is not in.
+
+Public entry points (drop-in execution of what the reference only costs):
+
+* ``attention_forward(plan, schedule, q, k, v)`` — LocalTask + RingRound
+  attention for this rank (reference simulator.py:124-188 charges it);
+* ``remap_forward(layout, x)`` / ``remap_inverse(layout, y)`` — the
+  attention<->linear token remap (simulator.py:282-302, remapping.py:187-255);
+* ``ZeppelinLayer`` — plan + attention + remap for one batch.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import ops
+from .plan import build_plan
+from .program import RankProgram, build_rank_program
+from .remap import RemapLayout, remap_layout
+from .schedule import build_schedule
+from .worklist import WorkList
+
+
+class RankContext:
+    """Rank identity, process group, streams and reusable device workspaces."""
+
+    def __init__(self, rank: int = 0, world: int = 1, device: torch.device | None = None, group=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("zeppelin-b200 executes on CUDA devices only (no CPU fallback)")
+        self.rank = rank
+        self.world = world
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.group = group
+        self.comm_stream = torch.cuda.Stream(self.device) if world > 1 else None
+        self._ws: dict[str, torch.Tensor] = {}
+
+    @classmethod
+    def from_env(cls) -> "RankContext":
+        if dist.is_available() and dist.is_initialized():
+            return cls(dist.get_rank(), dist.get_world_size())
+        return cls()
+
+    def workspace(self, name: str, shape, dtype) -> torch.Tensor:
+        numel = int(np.prod(shape))
+        buf = self._ws.get(name)
+        if buf is None or buf.numel() < numel or buf.dtype != dtype:
+            buf = torch.empty(max(numel, 1), dtype=dtype, device=self.device)
+            self._ws[name] = buf
+        return buf[:numel].view(*shape)
+
+
+@dataclass
+class _DevWork:
+    items: torch.Tensor
+    segs: torch.Tensor
+    n: int
+
+
+class DeviceProgram:
+    """A RankProgram's int32 tables, uploaded with one pinned H2D copy."""
+
+    def __init__(self, prog: RankProgram, device: torch.device):
+        self.prog = prog
+        chunks: list[np.ndarray] = []
+
+        def add(arr: np.ndarray) -> tuple[int, int]:
+            flat = np.ascontiguousarray(arr).view(np.int32).reshape(-1)
+            off = sum(c.size for c in chunks)
+            chunks.append(flat)
+            return off, flat.size
+
+        def add_work(wl: WorkList):
+            return add(wl.items), add(wl.segs), wl.n_items
+
+        local = add_work(prog.local)
+        rings = []
+        for rp in prog.rings:
+            pack = add(rp.pack_ranges)
+            rounds = [add_work(rr.work) for rr in rp.rounds]
+            rings.append((pack, rounds))
+        host = np.concatenate(chunks) if chunks else np.zeros(1, np.int32)
+        self.table = torch.from_numpy(host).pin_memory().to(device, non_blocking=True)
+
+        def view(span):
+            off, n = span
+            return self.table[off:off + n]
+
+        self.local = _DevWork(view(local[0]), view(local[1]), local[2])
+        self.rings = [(view(pack), [_DevWork(view(a), view(b), n) for a, b, n in rounds]) for pack, rounds in rings]
+        self.h2d_bytes = host.nbytes
+
+
+def ring_p2p_ops(rp, round_index: int, cur: torch.Tensor, nxt: torch.Tensor, group=None) -> list:
+    """Point-to-point ops after ring round ``round_index``: forward the held KV
+    set to position i+1 and receive the next one from i-1 (reference
+    attention_engine.py:247-251).  Zero-row transfers are skipped on both
+    sides (the counts are plan-determined)."""
+    ops_ = []
+    n_send, n_recv = rp.send_rows(round_index), rp.recv_rows(round_index)
+    if n_send:
+        ops_.append(dist.P2POp(dist.isend, cur[:n_send], rp.next_rank, group))
+    if n_recv:
+        ops_.append(dist.P2POp(dist.irecv, nxt[:n_recv], rp.prev_rank, group))
+    return ops_
+
+
+def _run_ring(ctx: RankContext, rp, dev_pack, dev_rounds, q, k, v, o, lse, scale):
+    hkv, d = k.shape[1], k.shape[2]
+    hq = q.shape[1]
+    cs = torch.cuda.current_stream()
+    xs = ctx.comm_stream
+    rows = max(rp.held_rows)
+    bufs = [ctx.workspace(f"ringkv{j}", (rows, 2, hkv, d), torch.bfloat16) for j in (0, 1)]
+    st_o = ctx.workspace("ring_state_o", (max(rp.state_rows, 1), hq, d), torch.float32)
+    st_ml = ctx.workspace("ring_state_ml", (2, hq, max(rp.state_rows, 1)), torch.float32)
+    n_pack = rp.pack_ranges.shape[0]
+    max_pack = int(rp.pack_ranges[:, 2].max()) if n_pack else 0
+    ops.copy_rows(bufs[0][:, 0], k, dev_pack, n_pack, max_pack)
+    ops.copy_rows(bufs[0][:, 1], v, dev_pack, n_pack, max_pack)
+    ready = torch.cuda.Event()
+    ready.record(cs)
+    done = None
+    g = rp.group_size
+    for r in range(g):
+        cur, nxt = bufs[r % 2], bufs[(r + 1) % 2]
+        nxt_ready = None
+        if r < g - 1:
+            xs.wait_event(ready)
+            if done is not None:
+                xs.wait_event(done)  # round r-1 finished reading nxt
+            with torch.cuda.stream(xs):
+                p2p = ring_p2p_ops(rp, r, cur, nxt, ctx.group)
+                if p2p:
+                    for req in dist.batch_isend_irecv(p2p):
+                        req.wait()
+                nxt_ready = torch.cuda.Event()
+                nxt_ready.record(xs)
+        if r > 0:
+            cs.wait_event(ready)
+        work = dev_rounds[r]
+        n_kv = rp.rounds[r].kv_rows
+        if work.n:
+            ops.attn_fwd(q, cur[:n_kv, 0], cur[:n_kv, 1], work.items, work.n, work.segs, o, lse,
+                         st_o, st_ml, softmax_scale=scale)
+        done = torch.cuda.Event()
+        done.record(cs)
+        if nxt_ready is not None:
+            ready = nxt_ready
+    if xs is not None:
+        cs.wait_stream(xs)  # buffers / sends complete before the next ring reuses them
+
+
+def attention_forward(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                      ctx: RankContext | None = None, program: RankProgram | None = None,
+                      device_program: DeviceProgram | None = None, softmax_scale: float | None = None,
+                      out: tuple[torch.Tensor, torch.Tensor] | None = None):
+    """This rank's attention (LocalTasks + every RingRound it takes part in).
+
+    q [A_r, Hq, 128], k/v [A_r, Hkv, 128] bf16 in the rank's attention layout
+    (plan.fragments[rank] rows in order).  Returns (o [A_r, Hq, 128] bf16,
+    lse [Hq, A_r] fp32)."""
+    ctx = ctx or RankContext.from_env()
+    hq = q.shape[1]
+    prog = program or build_rank_program(plan, schedule, ctx.rank, hq)
+    if q.shape[0] != prog.rows or k.shape[0] != prog.rows:
+        raise ValueError(f"rank {ctx.rank}: expected {prog.rows} attention-layout rows, got {q.shape[0]}")
+    devp = device_program or DeviceProgram(prog, q.device)
+    scale = 1.0 / math.sqrt(q.shape[2]) if softmax_scale is None else softmax_scale
+    if out is None:
+        o = torch.empty_like(q)
+        lse = torch.empty(hq, max(prog.rows, 1), dtype=torch.float32, device=q.device)
+    else:
+        o, lse = out
+    if devp.local.n:
+        ops.attn_fwd(q, k, v, devp.local.items, devp.local.n, devp.local.segs, o, lse, softmax_scale=scale)
+    for rp, (pack, rounds) in zip(prog.rings, devp.rings):
+        _run_ring(ctx, rp, pack, rounds, q, k, v, o, lse, scale)
+    return o, lse
+
+
+# ------------------------------------------------------------------ remap
+
+def _all_to_all(ctx: RankContext, out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits):
+    if ctx.world == 1:
+        return
+    dist.all_to_all_single(out, inp, output_split_sizes=[int(x) for x in out_splits],
+                           input_split_sizes=[int(x) for x in in_splits], group=ctx.group)
+
+
+def _copy_prefix(dst: torch.Tensor, src: torch.Tensor, n: int, ctx: RankContext) -> None:
+    if n <= 0 or dst.data_ptr() == src.data_ptr():
+        return
+    host = torch.empty((1, 3), dtype=torch.int32, pin_memory=True)  # caching host allocator
+    host[0, 0], host[0, 1], host[0, 2] = 0, 0, n
+    ops.copy_rows(dst, src, host.to(dst.device, non_blocking=True), 1, n)
+
+
+def _remap_move(ctx: RankContext, src: torch.Tensor, dst: torch.Tensor, slices) -> None:
+    kept, (s_lo, s_hi), (r_lo, r_hi), send, recv = slices
+    _copy_prefix(dst, src, kept, ctx)
+    if any(send) or any(recv):
+        _all_to_all(ctx, dst[r_lo:r_hi], src[s_lo:s_hi], recv, send)
+
+
+def remap_forward(layout: RemapLayout, x: torch.Tensor, ctx: RankContext | None = None,
+                  out: torch.Tensor | None = None) -> torch.Tensor:
+    """Attention layout [A_r, hidden] -> linear layout [B_r, hidden].
+
+    Kept rows stay in place (no copy when ``out`` shares ``x``'s storage); the
+    tail [B_r, A_r) leaves and received blocks land at [A_r, B_r) in sender
+    order — both contiguous, so NCCL's all-to-allv moves them directly."""
+    ctx = ctx or RankContext.from_env()
+    a, b = layout.attn_rows[ctx.rank], layout.linear_rows[ctx.rank]
+    if x.shape[0] != a:
+        raise ValueError(f"rank {ctx.rank}: remap input has {x.shape[0]} rows, layout says {a}")
+    y = out if out is not None else torch.empty((b,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+    _remap_move(ctx, x, y, layout.forward_slices(ctx.rank))
+    return y
+
+
+def remap_inverse(layout: RemapLayout, y: torch.Tensor, ctx: RankContext | None = None,
+                  out: torch.Tensor | None = None) -> torch.Tensor:
+    """Linear layout [B_r, hidden] -> attention layout [A_r, hidden] (exact inverse)."""
+    ctx = ctx or RankContext.from_env()
+    a, b = layout.attn_rows[ctx.rank], layout.linear_rows[ctx.rank]
+    if y.shape[0] != b:
+        raise ValueError(f"rank {ctx.rank}: remap input has {y.shape[0]} rows, layout says {b}")
+    x = out if out is not None else torch.empty((a,) + tuple(y.shape[1:]), dtype=y.dtype, device=y.device)
+    _remap_move(ctx, y, x, layout.inverse_slices(ctx.rank))
+    return x
+
+
+# ------------------------------------------------------------------ layer
+
+class ZeppelinLayer:
+    """Plan a batch and run attention + remap for this rank.
+
+    ``prepare(batch)`` runs the host planner (bit-identical to the reference)
+    and uploads this rank's work lists; ``forward(q, k, v)`` executes the
+    attention engine and the remap to the balanced linear layout;
+    ``backward_layout(y)`` restores the attention layout."""
+
+    def __init__(self, cluster, ctx: RankContext | None = None, n_heads: int = 32, n_kv_heads: int = 8,
+                 head_dim: int = 128):
+        self.cluster = cluster
+        self.ctx = ctx or RankContext.from_env()
+        self.n_heads, self.n_kv_heads, self.head_dim = n_heads, n_kv_heads, head_dim
+        self.plan = self.schedule = self.program = self.device_program = None
+
+    def prepare(self, batch):
+        self.plan = build_plan(batch, self.cluster)
+        self.schedule = build_schedule(self.plan)
+        self.program = build_rank_program(self.plan, self.schedule, self.ctx.rank, self.n_heads)
+        self.device_program = DeviceProgram(self.program, self.ctx.device)
+        return self.plan
+
+    @property
+    def layout(self) -> RemapLayout:
+        return self.program.remap
+
+    def attention(self, q, k, v):
+        return attention_forward(self.plan, self.schedule, q, k, v, self.ctx, self.program, self.device_program)
+
+    def forward(self, q, k, v):
+        o, lse = self.attention(q, k, v)
+        y = remap_forward(self.layout, o.view(o.shape[0], -1), self.ctx)
+        return o, lse, y
+
+    def backward_layout(self, y):
+        return remap_inverse(self.layout, y, self.ctx)

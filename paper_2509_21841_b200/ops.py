@@ -17,6 +17,26 @@ from .worklist import QueryFragment, WorkList, build_worklist
 
 HEAD_DIM = 128
 
+# Instrumentation: number of native kernel launches issued, and an optional
+# hook that receives CUDA events bracketing each attention launch (bench.py
+# uses it to time the dominant kernel on its own stream).
+_launches = 0
+_hook = None
+
+
+def reset_launch_count() -> None:
+    global _launches
+    _launches = 0
+
+
+def launch_count() -> int:
+    return _launches
+
+
+def set_launch_hook(fn) -> None:
+    global _hook
+    _hook = fn
+
 
 def _stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
     s = stream if stream is not None else torch.cuda.current_stream()
@@ -62,9 +82,17 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, items: torch.Ten
     st_o = state_o.data_ptr() if state_o is not None else None
     st_ml = state_ml.data_ptr() if state_ml is not None else None
     st_rows = int(state_o.shape[0]) if state_o is not None else 0
+    global _launches
+    _launches += 1
+    if _hook is not None:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
     _native.call("zp_attn_fwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), tq, tk, k.stride(0),
                  hq, hkv, d, o.data_ptr(), lse.data_ptr(), lse.stride(0), items.data_ptr(),
                  n_items, segs.data_ptr(), st_o, st_ml, st_rows, scale, _stream_ptr(stream))
+    if _hook is not None:
+        ev1.record()
+        _hook("zp_attn_fwd", ev0, ev1)
 
 
 def local_fragments(seqlens: list[int] | np.ndarray, row0: int = 0) -> list[QueryFragment]:
@@ -97,7 +125,9 @@ def copy_rows(dst: torch.Tensor, src: torch.Tensor, ranges: torch.Tensor, n_rang
               max_rows: int, stream: torch.cuda.Stream | None = None) -> None:
     """dst[d0:d0+n] = src[s0:s0+n] for each (d0, s0, n) row of the int32
     device table ``ranges``; rows are the leading dimension of both tensors."""
+    global _launches
     _require_cuda(dst, src, ranges)
+    _launches += 1
     row_bytes = src[0].numel() * src.element_size() if src.shape[0] else dst[0].numel() * dst.element_size()
     _native.call("zp_copy_rows", dst.data_ptr(), dst.stride(0) * dst.element_size(), src.data_ptr(),
                  src.stride(0) * src.element_size(), row_bytes, ranges.data_ptr(), n_ranges,

@@ -1,0 +1,179 @@
+"""Per-rank execution program: plan + schedule -> device work lists.
+
+Pure host logic (integers only), shared by the CUDA executor (``engine.py``)
+and the multi-process CPU tests.  For one rank it fixes
+
+* the attention layout: the rank's fragments in plan order (reference
+  ``partitioner.py:579-580``), each a contiguous run of rows;
+* the LocalTask work list (``attention_engine.py:260-265``);
+* for every ring the rank belongs to, in ``schedule.rings()`` order
+  (``attention_engine.py:266-271``): the ring KV buffer layout of every
+  position, the rows this rank packs into its own buffer, the send / receive
+  peers (KV moves position i -> i+1, ``attention_engine.py:247-251``) and one
+  work list per round against the KV held from position (i - r) mod g
+  (``attention_engine.py:229-244``), with partial-state flags so the rounds
+  compose into one exact online softmax;
+* the remap permutation (``remap.RemapLayout``).
+
+Every per-round work list's exact pair count is checked against the
+schedule's ``compute_pairs`` when the program is built.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .remap import RemapLayout, remap_layout
+from .schedule import LOCAL, AttentionSchedule, RingSchedule, ring_source
+from .worklist import (ITEM_LOAD_STATE, ITEM_STORE_STATE, QueryFragment, WorkList, build_worklist,
+                       tile_visible_pairs, TILE)
+
+
+@dataclass
+class RingRoundProgram:
+    round_index: int
+    src_position: int
+    kv_rows: int            # rows of the KV set held this round
+    work: WorkList
+
+
+@dataclass
+class RingProgram:
+    ring_index: int                     # index in schedule.rings()
+    members: tuple[int, ...]
+    position: int
+    next_rank: int
+    prev_rank: int
+    held_rows: list[int]                # KV rows held by each position
+    pack_ranges: np.ndarray             # int32 [n, 3]: (buf_row, layout_row, n_rows)
+    state_rows: int                     # partial-state rows this rank needs for the ring
+    rounds: list[RingRoundProgram] = field(default_factory=list)
+
+    @property
+    def group_size(self) -> int:
+        return len(self.members)
+
+    def send_rows(self, round_index: int) -> int:
+        """Rows forwarded to next_rank after round ``round_index``."""
+        return self.held_rows[ring_source(self.position, round_index, self.group_size)]
+
+    def recv_rows(self, round_index: int) -> int:
+        """Rows arriving from prev_rank for round ``round_index + 1``."""
+        return self.held_rows[ring_source(self.position, round_index + 1, self.group_size)]
+
+
+@dataclass
+class RankProgram:
+    rank: int
+    world: int
+    rows: int                           # A_rank, attention-layout rows
+    frag_rows: dict[tuple[int, int], int]  # (sid, start) -> layout row
+    local: WorkList
+    rings: list[RingProgram]
+    remap: RemapLayout
+    n_head_pairs: int
+
+    @property
+    def max_held_rows(self) -> int:
+        return max((max(r.held_rows) for r in self.rings), default=0)
+
+    @property
+    def max_state_rows(self) -> int:
+        return max((r.state_rows for r in self.rings), default=0)
+
+    def pairs_per_head(self) -> int:
+        return self.local.pairs_per_head + sum(rr.work.pairs_per_head for r in self.rings for rr in r.rounds)
+
+
+def _ring_buffer_rows(ring_sched: RingSchedule) -> list[dict[tuple[int, int], int]]:
+    """Per position: (sid, start) -> row in that position's KV buffer
+    (sequences by id, ranges in order)."""
+    ring = ring_sched.ring
+    out = []
+    for p in range(ring.group_size):
+        at, rows = 0, {}
+        for seq in ring.sequences:
+            for a, b in seq.ranges_by_position[p]:
+                rows[(seq.sequence_id, a)] = at
+                at += b - a
+        out.append(rows)
+    return out
+
+
+def build_rank_program(plan, schedule: AttentionSchedule, rank: int, n_heads: int,
+                       remap=None) -> RankProgram:
+    n_hp = n_heads // 2
+    frag_rows: dict[tuple[int, int], int] = {}
+    at = 0
+    local_frags: list[QueryFragment] = []
+    for f in plan.fragments[rank]:
+        frag_rows[(f.sequence_id, f.start)] = at
+        if plan.zone_of.get(f.sequence_id) == LOCAL or f.micro_batch > 0:
+            local_frags.append(QueryFragment(row0=at, pos0=0, length=f.tokens, segs=[(at, 0, f.tokens)]))
+        at += f.tokens
+    local = build_worklist(local_frags, n_hp)
+    want = sum(t.compute_pairs for t in schedule.local_tasks if t.rank == rank)
+    if local.pairs_per_head != want:
+        raise AssertionError(f"rank {rank}: local work list covers {local.pairs_per_head} pairs, schedule says {want}")
+
+    rings: list[RingProgram] = []
+    for ri, rs in enumerate(schedule.rings()):
+        ring = rs.ring
+        if rank not in ring.members:
+            continue
+        g = ring.group_size
+        i = ring.members.index(rank)
+        buf_rows = _ring_buffer_rows(rs)
+        held = [ring.kv_tokens(p) for p in range(g)]
+        pack = [(buf_rows[i][(s.sequence_id, a)], frag_rows[(s.sequence_id, a)], b - a)
+                for s in ring.sequences for a, b in s.ranges_by_position[i]]
+        # this rank's query fragments of the ring, with compact state rows
+        qf: list[tuple[int, int, int, int, int]] = []  # (sid, layout_row, pos0, len, state_row0)
+        srow = 0
+        for s in ring.sequences:
+            for a, b in s.ranges_by_position[i]:
+                qf.append((s.sequence_id, frag_rows[(s.sequence_id, a)], a, b - a, srow))
+                srow += b - a
+        seq_by_id = {s.sequence_id: s for s in ring.sequences}
+
+        def segs_for(sid: int, src: int) -> list[tuple[int, int, int]]:
+            return [(buf_rows[src][(sid, c)], c, d - c) for c, d in seq_by_id[sid].ranges_by_position[src]]
+
+        # visibility of every query tile in every round -> first / last round
+        vis = []
+        for sid, _, a, n, _ in qf:
+            p0 = a + np.arange(0, n, TILE)
+            ln = np.minimum(TILE, n - np.arange(0, n, TILE))
+            vis.append(np.stack([tile_visible_pairs(p0, ln, segs_for(sid, ring_source(i, r, g))) > 0
+                                 for r in range(g)]))
+        prog = RingProgram(ring_index=ri, members=ring.members, position=i,
+                           next_rank=ring.members[(i + 1) % g], prev_rank=ring.members[(i - 1) % g],
+                           held_rows=held, pack_ranges=np.asarray(pack, dtype=np.int32).reshape(-1, 3),
+                           state_rows=srow)
+        for r in range(g):
+            src = ring_source(i, r, g)
+            frags = [QueryFragment(row0=row, pos0=a, length=n, segs=segs_for(sid, src), state_row0=st)
+                     for sid, row, a, n, st in qf]
+
+            def flags(fi, p0, ln, r=r):
+                v = vis[fi]
+                seen_before = v[:r].any(axis=0)
+                seen_after = v[r + 1:].any(axis=0)
+                return np.where(seen_before, ITEM_LOAD_STATE, 0) | np.where(seen_after, ITEM_STORE_STATE, 0)
+
+            wl = build_worklist(frags, n_hp, tile_flags=flags)
+            expect = rs.rounds[i][r].compute_pairs
+            if wl.pairs_per_head != expect:
+                raise AssertionError(f"rank {rank} ring {ring.members} round {r}: work list covers "
+                                     f"{wl.pairs_per_head} pairs, schedule says {expect}")
+            prog.rounds.append(RingRoundProgram(round_index=r, src_position=src, kv_rows=held[src], work=wl))
+        rings.append(prog)
+
+    if remap is None:
+        remap = remap_layout(plan.tokens_per_rank)
+    elif not isinstance(remap, RemapLayout):
+        remap = remap_layout(plan.tokens_per_rank, remap)
+    return RankProgram(rank=rank, world=plan.num_ranks, rows=at, frag_rows=frag_rows, local=local,
+                       rings=rings, remap=remap, n_head_pairs=n_hp)

@@ -275,6 +275,18 @@ class RemapLayout:
     def moved_rows(self) -> int:
         return int(self.matrix.sum())
 
+    def forward_slices(self, rank: int):
+        """(kept rows, attention-layout rows sent [lo, hi), linear-layout rows
+        received [lo, hi), send counts per receiver, recv counts per sender)."""
+        a, b = self.attn_rows[rank], self.linear_rows[rank]
+        return (min(a, b), (b, max(a, b)), (a, max(a, b)), self.send_counts(rank), self.recv_counts(rank))
+
+    def inverse_slices(self, rank: int):
+        """Mirror of forward_slices for the linear -> attention direction:
+        (kept, linear rows sent, attention rows received, send counts, recv counts)."""
+        a, b = self.attn_rows[rank], self.linear_rows[rank]
+        return (min(a, b), (a, max(a, b)), (b, max(a, b)), self.recv_counts(rank), self.send_counts(rank))
+
     def source_of_linear_rows(self, rank: int) -> list[tuple[int, int, int]]:
         """(src_rank, src_row0, n) blocks composing rank's linear layout, in order."""
         blocks = [(rank, 0, self.kept(rank))] if self.kept(rank) else []

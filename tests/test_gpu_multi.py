@@ -1,0 +1,73 @@
+"""Multi-GPU executor (NCCL ring exchange + all-to-allv remap), one process per
+GPU, against the fp64 oracle.  Needs >= 2 B200s; skipped otherwise."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, lengths, results):
+    import torch.distributed as dist
+    from oracle import attention as OA
+    from oracle import remap as OR
+    from paper_2509_21841_b200 import engine, plan as P, schedule as S, remap as M
+    from paper_2509_21841_b200.batch import SequenceBatch
+    from paper_2509_21841_b200.cluster import single_box
+    from paper_2509_21841_b200.emulate import gather_rank
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        batch = SequenceBatch(tuple(enumerate(lengths)))
+        cluster = single_box(world, batch.total_tokens)
+        plan = P.build_plan(batch, cluster)
+        sched = S.build_schedule(plan)
+        g = torch.Generator().manual_seed(1)
+        seqs = sorted(plan.sequence_lengths.items())
+        sq = {s: torch.randn(n, 32, 128, generator=g).to(torch.bfloat16) for s, n in seqs}
+        sk = {s: torch.randn(n, 8, 128, generator=g).to(torch.bfloat16) for s, n in seqs}
+        sv = {s: torch.randn(n, 8, 128, generator=g).to(torch.bfloat16) for s, n in seqs}
+        ctx = engine.RankContext(rank, world)
+        q, k, v = (gather_rank(x, plan, rank, "cuda") for x in (sq, sk, sv))
+        o, lse = engine.attention_forward(plan, sched, q, k, v, ctx)
+        lay = M.remap_layout(plan.tokens_per_rank, M.solve_remap(plan.tokens_per_rank, M.cost_matrix(cluster)))
+        ids = torch.stack([torch.full((q.shape[0],), rank, dtype=torch.int32),
+                           torch.arange(q.shape[0], dtype=torch.int32)], 1)
+        ids = torch.cat([ids, torch.zeros(q.shape[0], 2, dtype=torch.int32)], 1).cuda()  # 16-byte rows
+        y = engine.remap_forward(lay, ids, ctx)
+        back = engine.remap_inverse(lay, y, ctx)
+        torch.cuda.synchronize()
+        f64 = lambda m: {s: t.double().numpy() for s, t in m.items()}  # noqa: E731
+        ref, _ = OA.run_plan(plan, sched, f64(sq), f64(sk), f64(sv), 128 ** -0.5)
+        err = float(np.abs(o.float().cpu().numpy() - ref[rank][0]).max()) if q.shape[0] else 0.0
+        want = OR.source_map(list(lay.attn_rows), lay.matrix)[rank]
+        perm_ok = bool(np.array_equal(y[:, :2].cpu().numpy(), want))
+        back_ok = bool(torch.equal(back, ids))
+        results[rank] = (err, perm_ok, back_ok, len(plan.ring_groups))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("lengths", [[6000, 300, 1200, 40, 700], [9000, 2000, 2000, 64]])
+def test_multi_gpu_attention_and_remap(lengths):
+    world = min(torch.cuda.device_count(), 4)
+    with mp.Manager() as mgr:
+        res = mgr.dict()
+        mp.spawn(_worker, args=(world, _port(), lengths, res), nprocs=world, join=True)
+        res = dict(res)
+    assert sorted(res) == list(range(world))
+    for rank, (err, perm_ok, back_ok, nrings) in res.items():
+        assert err <= 2e-2 and perm_ok and back_ok, res

@@ -1,0 +1,125 @@
+"""Per-rank programs (work lists, ring buffers, exchange peers, remap slices)
+interpreted on the CPU against the oracle — the host half of the executor."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import attention as OA
+from oracle import remap as OR
+from oracle import worklist as OW
+from paper_2509_21841_b200 import plan as P, schedule as S, remap as M, workloads as W
+from paper_2509_21841_b200.batch import SequenceBatch
+from paper_2509_21841_b200.cluster import ClusterSpec
+from paper_2509_21841_b200.program import build_rank_program
+
+
+def simulate(plan, hq=4, hkv=2, d=16, seed=0):
+    """Run every rank's program with an in-process ring exchange."""
+    sched = S.build_schedule(plan)
+    lengths = sorted(plan.sequence_lengths.items())
+    rng = np.random.default_rng(seed)
+    sq = {s: rng.standard_normal((n, hq, d)) for s, n in lengths}
+    sk = {s: rng.standard_normal((n, hkv, d)) for s, n in lengths}
+    sv = {s: rng.standard_normal((n, hkv, d)) for s, n in lengths}
+    progs = [build_rank_program(plan, sched, r, hq) for r in range(plan.num_ranks)]
+    q = [OA.gather_rank(sq, plan, r) for r in range(plan.num_ranks)]
+    k = [OA.gather_rank(sk, plan, r) for r in range(plan.num_ranks)]
+    v = [OA.gather_rank(sv, plan, r) for r in range(plan.num_ranks)]
+    outs = []
+    for r, pr in enumerate(progs):
+        n = pr.rows
+        o = np.zeros((n, hq, d))
+        lse = np.full((hq, n), -np.inf)
+        if n:
+            OW.run_items(pr.local.items, pr.local.segs, q[r], k[r], v[r], o, lse, None, d ** -0.5)
+        outs.append((o, lse))
+    # rings in global order; each member packs, then KV rotates i -> i+1
+    for ri, rs in enumerate(sched.rings()):
+        members = rs.ring.members
+        g = len(members)
+        rp = {m: next(x for x in progs[m].rings if x.ring_index == ri) for m in members}
+        held = {}
+        for m in members:
+            p = rp[m]
+            buf = np.zeros((max(p.held_rows), 2, hkv, d))
+            for dst, src, cnt in p.pack_ranges:
+                buf[dst:dst + cnt, 0] = k[m][src:src + cnt]
+                buf[dst:dst + cnt, 1] = v[m][src:src + cnt]
+            held[m] = buf
+        states = {m: OW.State(max(rp[m].state_rows, 1), hq, d) for m in members}
+        for rnd in range(g):
+            for m in members:
+                p = rp[m]
+                rr = p.rounds[rnd]
+                kv = held[m][:rr.kv_rows]
+                OW.run_items(rr.work.items, rr.work.segs, q[m], kv[:, 0], kv[:, 1], *outs[m], states[m], d ** -0.5)
+            if rnd < g - 1:
+                nxt = {}
+                for m in members:
+                    p = rp[m]
+                    assert p.send_rows(rnd) == rp[p.next_rank].recv_rows(rnd)
+                    nxt[p.next_rank] = held[m][:p.send_rows(rnd)].copy()
+                held = nxt
+    return sched, outs, (sq, sk, sv)
+
+
+def check(plan, **kw):
+    sched, outs, (sq, sk, sv) = simulate(plan, **kw)
+    d = next(iter(sq.values())).shape[2]
+    ref, _ = OA.run_plan(plan, sched, sq, sk, sv, d ** -0.5)
+    for (o, l), (ro, rl) in zip(outs, ref):
+        assert np.abs(o - ro).max() < 1e-10
+        assert np.abs(l - rl).max() < 1e-10
+
+
+def test_c1_program_matches_oracle():
+    check(P.build_plan(W.c1_batch(), W.c1_cluster()))
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_plans_program_matches_oracle(seed):
+    rng = np.random.default_rng(100 + seed)
+    g = int(rng.choice([2, 3, 4, 5]))
+    lengths = [int(x) for x in rng.integers(1, 400, size=int(rng.integers(2, 9)))]
+    lengths[int(rng.integers(len(lengths)))] = int(rng.integers(300, 900))
+    total = sum(lengths)
+    plan = P.build_plan(SequenceBatch(tuple(enumerate(lengths))), ClusterSpec(1, g, -(-total * 105 // (100 * g)), 1.0, 1.0))
+    check(plan, seed=seed)
+
+
+def test_programs_build_for_bench_configs():
+    """C3 / C4 / C5 plans at G = 2, 4, 8: per-round pair counts match the
+    schedule (asserted inside build_rank_program) and remap slices tile."""
+    for g in (2, 4, 8):
+        for batch in (W.c3_batch(g), W.c4_batch()):
+            plan = P.build_plan(batch, W.cluster_for(batch, g))
+            sched = S.build_schedule(plan)
+            res = M.solve_remap(plan.tokens_per_rank, M.cost_matrix(W.cluster_for(batch, g)))
+            total_pairs = 0
+            for r in range(g):
+                pr = build_rank_program(plan, sched, r, 32, res)
+                total_pairs += pr.pairs_per_head()
+                kept, (s0, s1), (r0, r1), send, recv = pr.remap.forward_slices(r)
+                assert s1 - s0 == sum(send) and r1 - r0 == sum(recv)
+            assert total_pairs == sum(S.causal_pairs(n) for _, n in batch.sequences)
+
+
+GOLDEN_PERM = os.path.join(os.path.dirname(__file__), "golden", "remap_permutation.json")
+
+
+def test_remap_permutation_golden():
+    """R3 row rule pinned: for each case, the (src rank, src row) of every
+    linear-layout row (run-length encoded) equals the committed fixture."""
+    doc = json.load(open(GOLDEN_PERM))
+    for case in doc["cases"]:
+        lay = M.remap_layout(case["counts"])
+        assert lay.matrix.tolist() == case["matrix"]
+        for r, blocks in enumerate(case["blocks"]):
+            assert [list(b) for b in lay.source_of_linear_rows(r)] == blocks
+        src = OR.source_map(case["counts"], lay.matrix)
+        for r, blocks in enumerate(case["blocks"]):
+            want = np.concatenate([np.stack([np.full(n, s), np.arange(o, o + n)], 1) for s, o, n in blocks]) \
+                if blocks else np.zeros((0, 2))
+            assert np.array_equal(src[r], want)
