@@ -14,7 +14,7 @@ import threading
 
 _LIB_NAME = "libzp_b200.so"
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, _LIB_NAME)
+LIB_PATH = os.environ.get("ZP_LIB_PATH") or os.path.join(_HERE, _LIB_NAME)  # override: experiments only
 
 _lock = threading.Lock()
 _lib: ctypes.CDLL | None = None

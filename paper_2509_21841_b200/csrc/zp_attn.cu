@@ -90,6 +90,64 @@ struct TileCursor {
   __device__ __forceinline__ int valid() const { return min(kBN, g.len - ti * kBN); }
 };
 
+#ifndef ZP_EMU_OF8
+#define ZP_EMU_OF8 1
+#endif
+constexpr float kRescaleLog2 = 8.0f;     // lazy-rescale threshold (log2 units)
+constexpr int kEmuOf8 = ZP_EMU_OF8;      // column pairs per 8 whose exp2 runs on the FMA pipe
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// 2^x for a pair on the FMA pipe: round-to-nearest split x = j + f (magic
+// constant 1.5*2^23), degree-3 minimax polynomial for 2^f on [-1/2, 1/2]
+// (max rel. error 7.5e-5, far below bf16's 3.9e-3), exponent add for 2^j.
+// x is clamped at -125 so the exponent add never underflows (2^-125 ~ 0).
+__device__ __forceinline__ float2 exp2_poly(float2 x) {
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 y = __fadd2_rn(x, magic);
+  const float2 j = __fadd2_rn(y, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __ffma2_rn(j, make_float2(-1.f, -1.f), x);
+  float2 p = __ffma2_rn(make_float2(0.055171608583694395f, 0.055171608583694395f), f,
+                        make_float2(0.2426111175727868f, 0.2426111175727868f));
+  p = __ffma2_rn(p, f, make_float2(0.6932609966238247f, 0.6932609966238247f));
+  p = __ffma2_rn(p, f, make_float2(0.9999280741082696f, 0.9999280741082696f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(y.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(y.y) << 23)));
+}
+
+// P = 2^(s*scale_log2 - m) for one 128-column row, packed to bf16x2 and
+// stored to the row's P columns in TMEM; row sum accumulated in two float2.
+// kEmu: a fixed share of column pairs takes the FMA-pipe exp2 (never on
+// masked tiles: -inf must give exactly 0).
+template <bool kEmu>
+__device__ __forceinline__ void exp_tile(const float (&s)[128], float2 sl2x2, float2 negm, uint32_t tP,
+                                         float2& acc0, float2& acc1) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int v = 0; v < 16; ++v) {
+      const float2 x = __ffma2_rn(make_float2(s[c * 32 + 2 * v], s[c * 32 + 2 * v + 1]), sl2x2, negm);
+      float2 p;
+      if (kEmu && ((c * 16 + v) & 7) < kEmuOf8) {
+        p = exp2_poly(x);
+      } else {
+        p.x = ex2(x.x);
+        p.y = ex2(x.y);
+      }
+      if (v & 1) acc1 = __fadd2_rn(acc1, p); else acc0 = __fadd2_rn(acc0, p);
+      pk[v] = pack_bf16(p.x, p.y);
+    }
+    tmem_st16(tP + c * 16, pk);
+  }
+}
+
 // Descriptor start addresses are in 16-byte units in the low 14 bits, so a
 // byte offset inside shared memory is added to a base descriptor as off>>4.
 __device__ __forceinline__ void issue_qk(uint32_t d_tmem, uint64_t q_desc, uint64_t k_desc,
@@ -276,56 +334,75 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(bar(B_SFULL + t), uint32_t(j) & 1);
         tc_fence_after();
         float s[128];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t r[32];
-          tmem_ld32(tS + c * 32, r);
+        {
+          uint32_t r0[32], r1[32], r2[32], r3[32];
+          tmem_ld32(tS + 0, r0);
+          tmem_ld32(tS + 32, r1);
+          tmem_ld32(tS + 64, r2);
+          tmem_ld32(tS + 96, r3);
           tmem_wait_ld();
 #pragma unroll
-          for (int v = 0; v < 32; ++v) s[c * 32 + v] = __uint_as_float(r[v]);
+          for (int v = 0; v < 32; ++v) {
+            s[v] = __uint_as_float(r0[v]);
+            s[32 + v] = __uint_as_float(r1[v]);
+            s[64 + v] = __uint_as_float(r2[v]);
+            s[96 + v] = __uint_as_float(r3[v]);
+          }
         }
         const int kpos0 = cur.pos();
         const int kv_valid = cur.valid();
-        if (kv_valid < kBN || kpos0 + kBN - 1 > it.q_pos0) {
+        const bool masked = kv_valid < kBN || kpos0 + kBN - 1 > it.q_pos0;
+        if (masked) {
           const int lim = min(kv_valid - 1, qpos - kpos0);  // last visible column
 #pragma unroll
           for (int c = 0; c < 128; ++c)
             if (c > lim) s[c] = -INFINITY;
         }
-        float mx = s[0];
+        // row max with 3-input max (FMNMX3)
+        float mx0 = fmax3(s[0], s[1], s[2]), mx1 = fmax3(s[3], s[4], s[5]);
 #pragma unroll
-        for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
-        const float m_new = fmaxf(m, mx * sl2);
+        for (int c = 6; c < 126; c += 4) {
+          mx0 = fmax3(mx0, s[c], s[c + 1]);
+          mx1 = fmax3(mx1, s[c + 2], s[c + 3]);
+        }
+        const float mx = fmax3(mx0, mx1, fmaxf(s[126], s[127])) * sl2;
+        // Lazy rescale: keep the reference max unless this tile exceeds it by
+        // more than 2^8; P <= 256 is exact enough in bf16 / fp32 and O, l stay
+        // consistent with the reference actually used.
+        const bool bump = mx > m + kRescaleLog2;
+        const float m_new = bump ? mx : m;
         const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-        const float alpha = ex2(m - m_use);
-        float sum = 0.f;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int v = 0; v < 16; ++v) {
-            const float p0 = ex2(fmaf(s[c * 32 + 2 * v], sl2, -m_use));
-            const float p1 = ex2(fmaf(s[c * 32 + 2 * v + 1], sl2, -m_use));
-            sum += p0 + p1;
-            pk[v] = pack_bf16(p0, p1);
-          }
-          tmem_st16(tP + c * 16, pk);
+        const float alpha = bump ? ex2(m - m_use) : 1.f;
+        const float2 sl2x2 = make_float2(sl2, sl2);
+        const float2 negm = make_float2(-m_use, -m_use);
+        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+        if (masked) {
+          exp_tile<false>(s, sl2x2, negm, tP, acc0, acc1);
+        } else {
+          exp_tile<true>(s, sl2x2, negm, tP, acc0, acc1);
         }
-        l = l * alpha + sum;
+        const float2 acc = __fadd2_rn(acc0, acc1);
+        l = l * alpha + (acc.x + acc.y);
         m = m_new;
-        // O_t must hold PV(j-1) before it is rescaled and before PV(j) is issued.
-        if (j > 0) {
-          mbar_wait(bar(B_ODONE + t), uint32_t(j - 1) & 1);
-          tc_fence_after();
-        }
-        if ((j > 0 || resume) && __any_sync(0xffffffffu, alpha != 1.f)) {
+        // O_t must hold PV(j-1) before it is rescaled (and PV(j) follows this
+        // thread's arrival), so wait only when this warp actually rescales.
+        if ((j > 0 || resume) && __any_sync(0xffffffffu, bump)) {
+          if (j > 0) {
+            mbar_wait(bar(B_ODONE + t), uint32_t(j - 1) & 1);
+            tc_fence_after();
+          }
+          const float2 a2 = make_float2(alpha, alpha);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             uint32_t r[32];
             tmem_ld32(tO + c * 32, r);
             tmem_wait_ld();
 #pragma unroll
-            for (int v = 0; v < 32; ++v) r[v] = __float_as_uint(__uint_as_float(r[v]) * alpha);
+            for (int v = 0; v < 16; ++v) {
+              const float2 o2 = __fmul2_rn(make_float2(__uint_as_float(r[2 * v]), __uint_as_float(r[2 * v + 1])), a2);
+              r[2 * v] = __float_as_uint(o2.x);
+              r[2 * v + 1] = __float_as_uint(o2.y);
+            }
             tmem_st32(tO + c * 32, r);
           }
         }
