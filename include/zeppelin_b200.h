@@ -82,12 +82,16 @@ typedef struct zp_kv_seg {
  * log).  Mask: key position <= query position (global in-sequence positions).
  * state_o: [state_rows, hq, 128] fp32 unnormalised accumulator, state_ml:
  * [2, hq, state_rows] fp32 (running max in log2 units, running sum); only
- * touched by items carrying ZP_ITEM_*_STATE.  Items must be device-resident. */
+ * touched by items carrying ZP_ITEM_*_STATE.  Items must be device-resident.
+ * workspace: >= ZP_ATTN_WORKSPACE_BYTES of device memory owned by the caller
+ * (the persistent CTAs' work counter; zeroed by the call on `stream`).  Items
+ * are claimed in list order, so pass them longest-first. */
+#define ZP_ATTN_WORKSPACE_BYTES 16
 ZP_API int zp_attn_fwd(const void* q, const void* k, const void* v, int q_rows, int kv_rows,
                 int kv_row_stride, int hq, int hkv, int head_dim, void* o, float* lse,
                 int lse_stride, const zp_attn_item* items, int n_items, const zp_kv_seg* segs,
                 float* state_o, float* state_ml, int state_rows, float softmax_scale,
-                void* stream);
+                void* workspace, void* stream);
 
 /* Row-range copy with 16-byte vector loads/stores.  For each range i:
  * dst rows [dst_row0[i], +n_rows[i]) <- src rows [src_row0[i], +n_rows[i]).

@@ -24,7 +24,7 @@ _c_int, _c_i64, _c_float, _vp = ctypes.c_int, ctypes.c_int64, ctypes.c_float, ct
 # name -> (restype, argtypes); mirrors include/zeppelin_b200.h exactly.
 SIGNATURES: dict[str, tuple] = {
     "zp_attn_fwd": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
-                             _vp, _vp, _c_int, _vp, _c_int, _vp, _vp, _vp, _c_int, _c_float, _vp]),
+                             _vp, _vp, _c_int, _vp, _c_int, _vp, _vp, _vp, _c_int, _c_float, _vp, _vp]),
     "zp_copy_rows": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_i64, _vp, _c_int, _c_int, _vp]),
     "zp_remap_push": (_c_int, [_vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                ctypes.c_int32, _c_int, _vp]),

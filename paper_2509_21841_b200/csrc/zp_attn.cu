@@ -36,7 +36,8 @@ constexpr uint32_t kSmemQ = 0;
 constexpr uint32_t kSmemK = 2 * kTileBytes;
 constexpr uint32_t kSmemV = 4 * kTileBytes;
 constexpr uint32_t kSmemBar = 6 * kTileBytes;
-constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;  // + barriers + alignment slack
+constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;  // + barriers/sched ring + alignment slack
+constexpr int kSchedSlots = 4;
 
 // barrier slots
 enum : int {
@@ -48,11 +49,16 @@ enum : int {
   B_SFULL = 9,   // +tile
   B_PFULL = 11,  // +tile
   B_ODONE = 13,  // +tile
-  B_COUNT = 15
+  B_QEMPTY = 15,
+  B_SCHED_FULL = 16,   // +slot (4): item index published by the producer
+  B_SCHED_EMPTY = 20,  // +slot (4): consumed by the MMA warp and 8 softmax warps
+  B_COUNT = 24
 };
 
 struct AttnArgs {
   const zp_attn_item* items;
+  int n_items;
+  int* next_item;  // global work counter (zeroed before the launch)
   const zp_kv_seg* segs;
   __nv_bfloat16* o;
   float* lse;
@@ -91,7 +97,7 @@ struct TileCursor {
 };
 
 #ifndef ZP_EMU_OF8
-#define ZP_EMU_OF8 1
+#define ZP_EMU_OF8 0
 #endif
 constexpr float kRescaleLog2 = 8.0f;     // lazy-rescale threshold (log2 units)
 constexpr int kEmuOf8 = ZP_EMU_OF8;      // column pairs per 8 whose exp2 runs on the FMA pipe
@@ -171,6 +177,28 @@ __device__ __forceinline__ void issue_pv(uint32_t d_tmem, uint32_t p_tmem, uint6
            (accumulate || kk > 0) ? 1u : 0u);
 }
 
+// Persistent, dynamically scheduled CTAs: the producer thread claims the next
+// item of the longest-first list with one atomicAdd (greedy LPT across SMs)
+// and publishes it to the MMA and softmax warps through a 4-slot smem ring.
+struct SchedRing {
+  uint32_t bar_full, bar_empty;  // barrier addresses of slot 0
+  volatile int* idx;             // kSchedSlots published item indices
+  __device__ __forceinline__ int consume(uint32_t k, bool arrive) const {
+    const uint32_t slot = k % kSchedSlots;
+    mbar_wait(bar_full + 8 * slot, (k / kSchedSlots) & 1);
+    const int v = idx[slot];
+    if (arrive) mbar_arrive(bar_empty + 8 * slot);
+    return v;
+  }
+};
+
+__device__ __forceinline__ int count_tiles(const zp_kv_seg* segs, const zp_attn_item& it) {
+  int n = 0;
+  TileCursor cur(segs, it.seg_begin, it.seg_count, it.q_pos0 + it.q_len - 1);
+  while (cur.next()) ++n;
+  return n;
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
@@ -182,20 +210,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t bar0 = sbase + kSmemBar;
   auto bar = [&](int i) -> uint32_t { return bar0 + 8u * uint32_t(i); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sgen + kSmemBar + 8 * B_COUNT);
+  const SchedRing ring{bar(B_SCHED_FULL), bar(B_SCHED_EMPTY),
+                       reinterpret_cast<volatile int*>(sgen + kSmemBar + 8 * B_COUNT + 16)};
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const zp_attn_item it = args.items[blockIdx.x];
-  const int max_qpos = it.q_pos0 + it.q_len - 1;
-  int n_tiles = 0;
-  {
-    TileCursor cur(args.segs, it.seg_begin, it.seg_count, max_qpos);
-    while (cur.next()) ++n_tiles;
-  }
-  const bool resume = (it.flags & ZP_ITEM_LOAD_STATE) != 0;
+  const int n_items = args.n_items;
 
   if (threadIdx.x == 0) {
     mbar_init(bar(B_QFULL), 1);
+    mbar_init(bar(B_QEMPTY), 1);
+    for (int k = 0; k < kSchedSlots; ++k) {
+      mbar_init(bar(B_SCHED_FULL + k), 1);
+      mbar_init(bar(B_SCHED_EMPTY + k), 9);  // MMA thread + one lane per softmax warp
+    }
     for (int s = 0; s < 2; ++s) {
       mbar_init(bar(B_KFULL + s), 1);
       mbar_init(bar(B_KEMPTY + s), 1);
@@ -213,39 +241,54 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int kvh = (2 * it.head_pair) / args.group;
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
-    if (n_tiles > 0 && warp == 0 && lane == 0) {
-      // ---------------- producer: Q once, then K_j / V_j per KV tile
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+    if (warp == 0 && lane == 0) {
+      // ---------------- producer: per item Q (2 heads), then K_j / V_j rings
       tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_last();
-      mbar_expect_tx(bar(B_QFULL), 2 * kTileBytes);
-      for (int t = 0; t < 2; ++t)
-        for (int b = 0; b < 2; ++b)
-          tma_load_2d(sbase + kSmemQ + t * kTileBytes + b * kBoxBytes, &tm_q, bar(B_QFULL),
-                      (2 * it.head_pair + t) * kHeadDim + b * 64, it.q_row0, pol_q);
-      TileCursor cur(args.segs, it.seg_begin, it.seg_count, max_qpos);
-      for (int j = 0; cur.next(); ++j) {
-                      const int st = j & 1;
-                      const uint32_t u = uint32_t(j >> 1);
-                      const int row = cur.row();
-                      if (j >= 2) mbar_wait(bar(B_KEMPTY + st), (u - 1) & 1);
-                      mbar_expect_tx(bar(B_KFULL + st), kTileBytes);
-                      for (int b = 0; b < 2; ++b)
-                        tma_load_2d(sbase + kSmemK + st * kTileBytes + b * kBoxBytes, &tm_k,
-                                    bar(B_KFULL + st), kvh * kHeadDim + b * 64, row, pol_kv);
-                      if (j >= 2) mbar_wait(bar(B_VEMPTY + st), (u - 1) & 1);
-                      mbar_expect_tx(bar(B_VFULL + st), kTileBytes);
-                      for (int b = 0; b < 2; ++b)
-                        tma_load_2d(sbase + kSmemV + st * kTileBytes + b * kBoxBytes, &tm_v,
-                                    bar(B_VFULL + st), kvh * kHeadDim + b * 64, row, pol_kv);
+      uint32_t jg = 0, qn = 0;
+      for (uint32_t k = 0;; ++k) {
+        const uint32_t slot = k % kSchedSlots;
+        if (k >= kSchedSlots) mbar_wait(bar(B_SCHED_EMPTY + slot), ((k / kSchedSlots) - 1) & 1);
+        const int idx = atomicAdd(args.next_item, 1);
+        ring.idx[slot] = idx;
+        mbar_arrive(bar(B_SCHED_FULL + slot));
+        if (idx >= n_items) break;
+        const zp_attn_item it = args.items[idx];
+        if (count_tiles(args.segs, it) == 0) continue;
+        const int kvh = (2 * it.head_pair) / args.group;
+        if (qn > 0) mbar_wait(bar(B_QEMPTY), (qn - 1) & 1);
+        mbar_expect_tx(bar(B_QFULL), 2 * kTileBytes);
+        for (int t = 0; t < 2; ++t)
+          for (int b = 0; b < 2; ++b)
+            tma_load_2d(sbase + kSmemQ + t * kTileBytes + b * kBoxBytes, &tm_q, bar(B_QFULL),
+                        (2 * it.head_pair + t) * kHeadDim + b * 64, it.q_row0, pol_q);
+        ++qn;
+        TileCursor cur(args.segs, it.seg_begin, it.seg_count, it.q_pos0 + it.q_len - 1);
+        for (; cur.next(); ++jg) {
+          const int st = jg & 1;
+          const uint32_t u = jg >> 1;
+          const int row = cur.row();
+          if (jg >= 2) mbar_wait(bar(B_KEMPTY + st), (u - 1) & 1);
+          mbar_expect_tx(bar(B_KFULL + st), kTileBytes);
+          for (int b = 0; b < 2; ++b)
+            tma_load_2d(sbase + kSmemK + st * kTileBytes + b * kBoxBytes, &tm_k, bar(B_KFULL + st),
+                        kvh * kHeadDim + b * 64, row, pol_kv);
+          if (jg >= 2) mbar_wait(bar(B_VEMPTY + st), (u - 1) & 1);
+          mbar_expect_tx(bar(B_VFULL + st), kTileBytes);
+          for (int b = 0; b < 2; ++b)
+            tma_load_2d(sbase + kSmemV + st * kTileBytes + b * kBoxBytes, &tm_v, bar(B_VFULL + st),
+                        kvh * kHeadDim + b * 64, row, pol_kv);
+        }
       }
-    } else if (n_tiles > 0 && warp == 1 && lane == 0) {
-      // ---------------- MMA issuer
+    } else if (warp == 1 && lane == 0) {
+      // ---------------- MMA issuer.  Global tile stream: at tile g it issues
+      // PV_t(g-1) then S_t(g) for t = 0, 1 (the S/P TMEM aliasing relies on
+      // tcgen05 MMAs executing in issue order).
       constexpr uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
       const uint32_t tS[2] = {tmem + 0, tmem + 128};
@@ -254,59 +297,101 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t k_desc0 = umma_desc_sw128(sbase + kSmemK, 16, 1024);
       const uint64_t v_desc0 = umma_desc_sw128(sbase + kSmemV, kBoxBytes, 1024);
       const uint64_t vk_step = kTileBytes >> 4;  // one 32 KB tile, in descriptor units
-      mbar_wait(bar(B_QFULL), 0);
-      mbar_wait(bar(B_KFULL + 0), 0);
-      tc_fence_after();
-      for (int t = 0; t < 2; ++t) {
-        issue_qk(tS[t], q_desc0 + vk_step * t, k_desc0, idesc_qk);
-        tc_commit(bar(B_SFULL + t));
+      uint32_t jg = 0, qn = 0;
+      bool prev_acc = false;  // accumulate flag of the pending PV (tile jg-1)
+      for (uint32_t k = 0;; ++k) {
+        const int idx = ring.consume(k, true);
+        if (idx >= n_items) break;
+        const zp_attn_item it = args.items[idx];
+        const int n = count_tiles(args.segs, it);
+        if (n == 0) continue;
+        const bool resume = (it.flags & ZP_ITEM_LOAD_STATE) != 0;
+        for (int j = 0; j < n; ++j, ++jg) {
+          const int st = jg & 1, pst = (jg - 1) & 1;
+          if (jg > 0) {
+            mbar_wait(bar(B_VFULL + pst), ((jg - 1) >> 1) & 1);
+            tc_fence_after();
+          }
+          if (j == 0) {
+            // item boundary: finish the previous item's PVs first so its
+            // epilogue is not held up by this item's Q load
+            if (jg > 0) {
+              for (int t = 0; t < 2; ++t) {
+                mbar_wait(bar(B_PFULL + t), (jg - 1) & 1);
+                tc_fence_after();
+                issue_pv(tO[t], tS[t] + 64, v_desc0 + vk_step * pst, idesc_pv, prev_acc);
+                tc_commit(bar(B_ODONE + t));
+              }
+            }
+            mbar_wait(bar(B_QFULL), qn & 1);
+            mbar_wait(bar(B_KFULL + st), (jg >> 1) & 1);
+            tc_fence_after();
+            for (int t = 0; t < 2; ++t) {
+              issue_qk(tS[t], q_desc0 + vk_step * t, k_desc0 + vk_step * st, idesc_qk);
+              tc_commit(bar(B_SFULL + t));
+            }
+          } else {
+            for (int t = 0; t < 2; ++t) {
+              mbar_wait(bar(B_PFULL + t), (jg - 1) & 1);
+              tc_fence_after();
+              issue_pv(tO[t], tS[t] + 64, v_desc0 + vk_step * pst, idesc_pv, prev_acc);
+              tc_commit(bar(B_ODONE + t));
+              if (t == 0) {
+                mbar_wait(bar(B_KFULL + st), (jg >> 1) & 1);
+                tc_fence_after();
+              }
+              issue_qk(tS[t], q_desc0 + vk_step * t, k_desc0 + vk_step * st, idesc_qk);
+              tc_commit(bar(B_SFULL + t));
+            }
+          }
+          if (jg > 0) tc_commit(bar(B_VEMPTY + pst));
+          tc_commit(bar(B_KEMPTY + st));
+          if (j == n - 1) tc_commit(bar(B_QEMPTY));  // Q free once this item's S MMAs land
+          prev_acc = resume || j > 0;
+        }
+        ++qn;
       }
-      tc_commit(bar(B_KEMPTY + 0));
-      for (int j = 1; j < n_tiles; ++j) {
-        const int st = j & 1, pst = (j - 1) & 1;
-        mbar_wait(bar(B_KFULL + st), uint32_t(j >> 1) & 1);
-        mbar_wait(bar(B_VFULL + pst), uint32_t((j - 1) >> 1) & 1);
+      if (jg > 0) {
+        const int pst = (jg - 1) & 1;
+        mbar_wait(bar(B_VFULL + pst), ((jg - 1) >> 1) & 1);
         tc_fence_after();
         for (int t = 0; t < 2; ++t) {
-          mbar_wait(bar(B_PFULL + t), uint32_t(j - 1) & 1);
+          mbar_wait(bar(B_PFULL + t), (jg - 1) & 1);
           tc_fence_after();
-          issue_pv(tO[t], tS[t] + 64, v_desc0 + vk_step * pst, idesc_pv, resume || (j - 1) > 0);
+          issue_pv(tO[t], tS[t] + 64, v_desc0 + vk_step * pst, idesc_pv, prev_acc);
           tc_commit(bar(B_ODONE + t));
-          issue_qk(tS[t], q_desc0 + vk_step * t, k_desc0 + vk_step * st, idesc_qk);
-          tc_commit(bar(B_SFULL + t));
         }
-        tc_commit(bar(B_KEMPTY + st));
-        tc_commit(bar(B_VEMPTY + pst));
-      }
-      const int jl = n_tiles - 1, pst = jl & 1;
-      mbar_wait(bar(B_VFULL + pst), uint32_t(jl >> 1) & 1);
-      tc_fence_after();
-      for (int t = 0; t < 2; ++t) {
-        mbar_wait(bar(B_PFULL + t), uint32_t(jl) & 1);
-        tc_fence_after();
-        issue_pv(tO[t], tS[t] + 64, v_desc0 + vk_step * pst, idesc_pv, resume || jl > 0);
-        tc_commit(bar(B_ODONE + t));
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
-    if (n_tiles > 0) {
-      // ---------------- softmax / correction / epilogue
-      const int t = (warp - 4) >> 2;
-      const int quad = warp & 3;
-      const int row = quad * 32 + lane;
-      const uint32_t lane_bits = uint32_t(quad * 32) << 16;
-      const uint32_t tS = tmem + lane_bits + uint32_t(t * 128);
-      const uint32_t tP = tS + 64;
-      const uint32_t tO = tmem + lane_bits + 256u + uint32_t(t * 128);
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    // ---------------- softmax / correction / epilogue (thread == row)
+    const int t = (warp - 4) >> 2;
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const uint32_t lane_bits = uint32_t(quad * 32) << 16;
+    const uint32_t tS = tmem + lane_bits + uint32_t(t * 128);
+    const uint32_t tP = tS + 64;
+    const uint32_t tO = tmem + lane_bits + 256u + uint32_t(t * 128);
+    const float sl2 = args.scale_log2;
+    uint32_t jg = 0;
+    for (uint32_t k = 0;; ++k) {
+      const int idx = ring.consume(k, false);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(B_SCHED_EMPTY + (k % kSchedSlots)));
+      if (idx >= n_items) break;
+      const zp_attn_item it = args.items[idx];
+      TileCursor cur(args.segs, it.seg_begin, it.seg_count, it.q_pos0 + it.q_len - 1);
+      if (count_tiles(args.segs, it) == 0) continue;
+      const bool resume = (it.flags & ZP_ITEM_LOAD_STATE) != 0;
       const int h = 2 * it.head_pair + t;
       const int qpos = it.q_pos0 + row;
-      const float sl2 = args.scale_log2;
+      const bool ok = row < it.q_len;
       float m = -INFINITY, l = 0.f;
 
       if (resume) {
+        // O_t is free: the previous item's epilogue (this thread) drained it.
         const int srow = it.state_row0 + row;
-        const bool ok = row < it.q_len;
         if (ok) {
           m = args.st_ml[size_t(h) * args.state_rows + srow];
           l = args.st_ml[size_t(args.hq + h) * args.state_rows + srow];
@@ -315,23 +400,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             reinterpret_cast<const float4*>(args.st_o + (size_t(srow) * args.hq + h) * kHeadDim);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          uint32_t r[32];
+          uint32_t rr[32];
 #pragma unroll
           for (int v = 0; v < 8; ++v) {
             float4 x = ok ? src[c * 8 + v] : make_float4(0.f, 0.f, 0.f, 0.f);
-            r[4 * v + 0] = __float_as_uint(x.x);
-            r[4 * v + 1] = __float_as_uint(x.y);
-            r[4 * v + 2] = __float_as_uint(x.z);
-            r[4 * v + 3] = __float_as_uint(x.w);
+            rr[4 * v + 0] = __float_as_uint(x.x);
+            rr[4 * v + 1] = __float_as_uint(x.y);
+            rr[4 * v + 2] = __float_as_uint(x.z);
+            rr[4 * v + 3] = __float_as_uint(x.w);
           }
-          tmem_st32(tO + c * 32, r);
+          tmem_st32(tO + c * 32, rr);
         }
         tmem_wait_st();
       }
 
-      TileCursor cur(args.segs, it.seg_begin, it.seg_count, max_qpos);
-      for (int j = 0; cur.next(); ++j) {
-        mbar_wait(bar(B_SFULL + t), uint32_t(j) & 1);
+      for (int j = 0; cur.next(); ++j, ++jg) {
+        mbar_wait(bar(B_SFULL + t), jg & 1);
         tc_fence_after();
         float s[128];
         {
@@ -384,26 +468,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float2 acc = __fadd2_rn(acc0, acc1);
         l = l * alpha + (acc.x + acc.y);
         m = m_new;
-        // O_t must hold PV(j-1) before it is rescaled (and PV(j) follows this
+        // O_t must hold PV(g-1) before it is rescaled (and PV(g) follows this
         // thread's arrival), so wait only when this warp actually rescales.
         if ((j > 0 || resume) && __any_sync(0xffffffffu, bump)) {
           if (j > 0) {
-            mbar_wait(bar(B_ODONE + t), uint32_t(j - 1) & 1);
+            mbar_wait(bar(B_ODONE + t), (jg - 1) & 1);
             tc_fence_after();
           }
           const float2 a2 = make_float2(alpha, alpha);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            uint32_t r[32];
-            tmem_ld32(tO + c * 32, r);
+            uint32_t rr[32];
+            tmem_ld32(tO + c * 32, rr);
             tmem_wait_ld();
 #pragma unroll
             for (int v = 0; v < 16; ++v) {
-              const float2 o2 = __fmul2_rn(make_float2(__uint_as_float(r[2 * v]), __uint_as_float(r[2 * v + 1])), a2);
-              r[2 * v] = __float_as_uint(o2.x);
-              r[2 * v + 1] = __float_as_uint(o2.y);
+              const float2 o2 = __fmul2_rn(make_float2(__uint_as_float(rr[2 * v]), __uint_as_float(rr[2 * v + 1])), a2);
+              rr[2 * v] = __float_as_uint(o2.x);
+              rr[2 * v + 1] = __float_as_uint(o2.y);
             }
-            tmem_st32(tO + c * 32, r);
+            tmem_st32(tO + c * 32, rr);
           }
         }
         tmem_wait_st();
@@ -411,24 +495,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(bar(B_PFULL + t));
       }
 
-      // ---------------- epilogue
-      mbar_wait(bar(B_ODONE + t), uint32_t(n_tiles - 1) & 1);
+      // ---------------- epilogue of this item (overlaps the next item's S MMAs)
+      mbar_wait(bar(B_ODONE + t), (jg - 1) & 1);
       tc_fence_after();
-      const bool ok = row < it.q_len;
       if (it.flags & ZP_ITEM_STORE_STATE) {
         const int srow = it.state_row0 + row;
         float4* dst = reinterpret_cast<float4*>(args.st_o + (size_t(srow) * args.hq + h) * kHeadDim);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          uint32_t r[32];
-          tmem_ld32(tO + c * 32, r);
+          uint32_t rr[32];
+          tmem_ld32(tO + c * 32, rr);
           tmem_wait_ld();
           if (ok) {
 #pragma unroll
             for (int v = 0; v < 8; ++v)
-              dst[c * 8 + v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                           __uint_as_float(r[4 * v + 2]),
-                                           __uint_as_float(r[4 * v + 3]));
+              dst[c * 8 + v] = make_float4(__uint_as_float(rr[4 * v]), __uint_as_float(rr[4 * v + 1]),
+                                           __uint_as_float(rr[4 * v + 2]),
+                                           __uint_as_float(rr[4 * v + 3]));
           }
         }
         if (ok) {
@@ -441,17 +524,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                            kHeadDim);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          uint32_t r[32];
-          tmem_ld32(tO + c * 32, r);
+          uint32_t rr[32];
+          tmem_ld32(tO + c * 32, rr);
           tmem_wait_ld();
           if (ok) {
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
               uint4 w;
-              w.x = pack_bf16(__uint_as_float(r[8 * v + 0]) * inv_l, __uint_as_float(r[8 * v + 1]) * inv_l);
-              w.y = pack_bf16(__uint_as_float(r[8 * v + 2]) * inv_l, __uint_as_float(r[8 * v + 3]) * inv_l);
-              w.z = pack_bf16(__uint_as_float(r[8 * v + 4]) * inv_l, __uint_as_float(r[8 * v + 5]) * inv_l);
-              w.w = pack_bf16(__uint_as_float(r[8 * v + 6]) * inv_l, __uint_as_float(r[8 * v + 7]) * inv_l);
+              w.x = pack_bf16(__uint_as_float(rr[8 * v + 0]) * inv_l, __uint_as_float(rr[8 * v + 1]) * inv_l);
+              w.y = pack_bf16(__uint_as_float(rr[8 * v + 2]) * inv_l, __uint_as_float(rr[8 * v + 3]) * inv_l);
+              w.z = pack_bf16(__uint_as_float(rr[8 * v + 4]) * inv_l, __uint_as_float(rr[8 * v + 5]) * inv_l);
+              w.w = pack_bf16(__uint_as_float(rr[8 * v + 6]) * inv_l, __uint_as_float(rr[8 * v + 7]) * inv_l);
               dst[c * 4 + v] = w;
             }
           }
@@ -479,7 +562,7 @@ extern "C" int zp_attn_fwd(const void* q, const void* k, const void* v, int q_ro
                            int kv_row_stride, int hq, int hkv, int head_dim, void* o, float* lse,
                            int lse_stride, const zp_attn_item* items, int n_items,
                            const zp_kv_seg* segs, float* state_o, float* state_ml,
-                           int state_rows, float softmax_scale, void* stream) {
+                           int state_rows, float softmax_scale, void* workspace, void* stream) {
   using namespace zp;
   if (head_dim != kHeadDim) return zp_fail(ZP_EINVAL, "zp_attn_fwd: head_dim must be 128");
   if (hq <= 0 || hkv <= 0 || hq % hkv != 0 || (hq / hkv) % 2 != 0)
@@ -488,7 +571,7 @@ extern "C" int zp_attn_fwd(const void* q, const void* k, const void* v, int q_ro
     return zp_fail(ZP_EINVAL, "zp_attn_fwd: bad sizes");
   if (n_items == 0) return ZP_OK;
   if (q_rows == 0 || kv_rows == 0) return zp_fail(ZP_EINVAL, "zp_attn_fwd: empty q or kv with items");
-  if (!q || !k || !v || !o || !lse || !items || !segs)
+  if (!q || !k || !v || !o || !lse || !items || !segs || !workspace)
     return zp_fail(ZP_EINVAL, "zp_attn_fwd: null pointer");
   if (zp_check_device() != ZP_OK) return ZP_ENODEV;
 
@@ -513,6 +596,8 @@ extern "C" int zp_attn_fwd(const void* q, const void* k, const void* v, int q_ro
   }
   AttnArgs a;
   a.items = items;
+  a.n_items = n_items;
+  a.next_item = reinterpret_cast<int*>(workspace);
   a.segs = segs;
   a.o = reinterpret_cast<__nv_bfloat16*>(o);
   a.lse = lse;
@@ -523,7 +608,13 @@ extern "C" int zp_attn_fwd(const void* q, const void* k, const void* v, int q_ro
   a.hq = hq;
   a.group = hq / hkv;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
-  attn_fwd_kernel<<<n_items, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(
+  static int sms = 0;
+  if (sms == 0) sms = zp_device_sm_count();
+  if (sms <= 0) return zp_fail(ZP_ENODEV, "zp_attn_fwd: cannot query SM count");
+  const int grid = n_items < sms ? n_items : sms;  // persistent: one CTA per SM
+  cudaError_t me = cudaMemsetAsync(workspace, 0, sizeof(int), reinterpret_cast<cudaStream_t>(stream));
+  if (me != cudaSuccess) return zp_fail_cuda(me, "zp_attn_fwd: workspace reset");
+  attn_fwd_kernel<<<grid, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(
       tq, tk, tv, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return zp_fail_cuda(e, "zp_attn_fwd: launch");

@@ -38,6 +38,19 @@ def set_launch_hook(fn) -> None:
     _hook = fn
 
 
+_workspaces: dict = {}
+
+
+def _workspace(device: torch.device) -> torch.Tensor:
+    """Per-device scratch for the attention scheduler counter (torch-owned)."""
+    key = (device.type, device.index)
+    ws = _workspaces.get(key)
+    if ws is None:
+        ws = torch.zeros(16, dtype=torch.uint8, device=device)
+        _workspaces[key] = ws
+    return ws
+
+
 def _stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
     s = stream if stream is not None else torch.cuda.current_stream()
     return int(s.cuda_stream)
@@ -89,7 +102,8 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, items: torch.Ten
         ev0.record()
     _native.call("zp_attn_fwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), tq, tk, k.stride(0),
                  hq, hkv, d, o.data_ptr(), lse.data_ptr(), lse.stride(0), items.data_ptr(),
-                 n_items, segs.data_ptr(), st_o, st_ml, st_rows, scale, _stream_ptr(stream))
+                 n_items, segs.data_ptr(), st_o, st_ml, st_rows, scale, _workspace(q.device).data_ptr(),
+                 _stream_ptr(stream))
     if _hook is not None:
         ev1.record()
         _hook("zp_attn_fwd", ev0, ev1)
