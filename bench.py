@@ -214,6 +214,10 @@ def run_gpu(args):
     busiest = max(range(world), key=lambda i: per_rank[i][2])
     moved = lay.moved_rows()
 
+    remap_stress = None
+    if world > 1 and not args.no_remap_stress:
+        remap_stress = run_remap_stress(ctx, dev, world, rank, args)
+
     # end to end through the public API with host buffers (pinned), rank-local
     e2e = None
     if not args.no_e2e:
@@ -271,6 +275,7 @@ def run_gpu(args):
             "attn_ms_per_step": per_rank[busiest][1],
             "aggregate_tflops": sum(r[2] for r in per_rank) * FLOP_PER_PAIR / (ms / 1e3) / 1e12,
         },
+        "remap_stress": remap_stress,
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "e2e": e2e,
@@ -332,6 +337,71 @@ def run_e2e(args, ctx, dev, rows, hq, hkv, d, host_plan, world, rank):
             "h2d_bytes_per_step": int((hq_.numel() + hk_.numel() + hv_.numel()) * 2),
             "d2h_bytes_per_step": int(ho_.numel() * 2),
             "api": "paper_2509_21841_b200.engine.attention_forward + remap_forward + remap_inverse"}
+
+
+def run_remap_stress(ctx, dev, world, rank, args, total=262144, iters=10):
+    """Config 4 (remap alone, hidden 4096 bf16, 256K tokens) on the two
+    declared stress layouts of SURVEY 8(d): S1 fan-out (rank 0 holds every
+    token) and S2 alternating (even ranks hold 2T/G, odd ranks none).  Both
+    the NCCL all-to-allv path and the fused peer-store kernel are timed
+    (forward remap, CUDA events, max over ranks); bandwidth is the busiest
+    sender's bytes / time against 900 GB/s nominal and 770 GB/s measured
+    per-direction NVLink."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_21841_b200 import engine
+    from paper_2509_21841_b200.remap import remap_layout
+
+    hidden = 4096
+    out = {}
+    layouts = {
+        "S1_fan_out": [total] + [0] * (world - 1),
+        "S2_alternating": [2 * total // world if i % 2 == 0 else 0 for i in range(world)],
+    }
+    for name, counts in layouts.items():
+        lay = remap_layout(counts)
+        a, b = lay.attn_rows[rank], lay.linear_rows[rank]
+        sent = [int(lay.matrix[i].sum()) * hidden * 2 for i in range(world)]
+        busiest = max(sent)
+        res = {"counts": counts, "rows_moved": lay.moved_rows(), "busiest_sender_bytes": busiest}
+        att = engine.PeerBuffer(ctx, max(lay.attn_rows), hidden)
+        lin = engine.PeerBuffer(ctx, max(lay.linear_rows), hidden)
+        att.buf.normal_()
+        x = att.buf[:a]
+        tabs = engine.push_tables(lay, rank, False, dev)
+        paths = {
+            "nccl_all_to_allv": lambda: engine.remap_forward(lay, x, ctx, out=lin.buf[:b]),
+            "fused_peer_store": lambda: engine.remap_push(lay, x, lin, ctx, tables=tabs),
+        }
+        for pname, fn in paths.items():
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(iters):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1) / iters], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            gbs = busiest / (ms / 1e3) / 1e9
+            res[pname] = {"ms": ms, "GB_per_s_busiest_sender": gbs, "frac_nvlink_900": gbs / 900.0,
+                          "frac_nvlink_770_measured": gbs / 770.0}
+        # exactness of the fused path against the NCCL path on these rows
+        y1 = engine.remap_forward(lay, x, ctx).clone()
+        y2 = engine.remap_push(lay, x, lin, ctx, tables=tabs)
+        torch.cuda.synchronize()
+        ok = torch.tensor([int(torch.equal(y1, y2))], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        res["fused_equals_nccl"] = bool(ok.item())
+        out[name] = res
+        del att, lin
+        torch.cuda.empty_cache()
+    return out
 
 
 # ---------------------------------------------------------------------------- CPU arm
@@ -424,6 +494,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-remap-stress", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "zeppelin":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

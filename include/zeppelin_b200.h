@@ -101,12 +101,19 @@ ZP_API int zp_copy_rows(void* dst, int64_t dst_stride_bytes, const void* src, in
                  int64_t row_bytes, const int32_t* ranges, int n_ranges, int max_rows_per_range,
                  void* stream);
 
-/* Fused remap push: for each destination d, rows [src_row0[d], +count[d]) of
- * `src` are stored directly into peer buffer dst_ptrs[d] (a device pointer
- * valid in this process, e.g. CUDA-IPC mapped) at row dst_row0[d].  Then the
- * kernel release-stores `epoch` into flags_ptrs[d][my_rank] and finally waits
- * until its own flag row (flags_ptrs[my_rank][s], s with expect[s]) reaches
- * `epoch`.  All arrays are device int64/int32 of length world. */
+/* Fused remap push (collective: every rank calls it with the same epoch).
+ * flags_ptrs[r] points at rank r's int32[2*world] flag block (IPC-mapped):
+ * [0,world) "done from sender s", [world,2*world) "ready from rank s".
+ *  1. ready: release-store `epoch` into every peer's ready slot, then wait
+ *     until each destination d (count[d] > 0) has announced `epoch` — so no
+ *     rank overwrites a buffer its owner is still reading;
+ *  2. push: rows [src_row0[d], +count[d]) of `src` are stored straight into
+ *     dst_ptrs[d] (a peer pointer valid in this process) at row dst_row0[d],
+ *     16-byte vector stores over NVLink;
+ *  3. done: release-store `epoch` into each destination's done slot, then
+ *     acquire-wait for `epoch` from every sender s with expect[s] != 0.
+ * Epochs must increase from call to call.  All tables are device arrays of
+ * length world (int64 pointers, int32 counts/rows). */
 ZP_API int zp_remap_push(const void* src, int64_t row_bytes, const int64_t* dst_ptrs,
                   const int32_t* src_row0, const int32_t* dst_row0, const int32_t* count,
                   const int64_t* flags_ptrs, const int32_t* expect, int world, int my_rank,

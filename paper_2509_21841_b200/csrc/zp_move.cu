@@ -75,25 +75,48 @@ __global__ void __launch_bounds__(kMoveThreads)
   __threadfence_system();
 }
 
-// One warp: publish `epoch` to every destination we wrote, then wait for the
-// epoch from every sender that writes to us.
-__global__ void remap_signal_kernel(const int64_t* __restrict__ flags_ptrs,
-                                    const int32_t* __restrict__ count,
-                                    const int32_t* __restrict__ expect, int world, int me,
-                                    int32_t epoch) {
+// Flag layout per rank (int32[2*world], IPC-shared): [0, world) "done" —
+// sender s finished storing epoch e into my buffer; [world, 2*world) "ready" —
+// rank s reached epoch e, so every earlier read of its buffers is complete.
+__device__ __forceinline__ void st_release_sys(int32_t* p, int32_t v) {
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int32_t ld_acquire_sys(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Entry handshake: tell every peer we reached `epoch`, then wait until every
+// rank we are about to store into has reached it too.
+__global__ void remap_ready_kernel(const int64_t* __restrict__ flags_ptrs,
+                                   const int32_t* __restrict__ count, int world, int me,
+                                   int32_t epoch) {
   __threadfence_system();
+  for (int d = threadIdx.x; d < world; d += blockDim.x)
+    if (d != me) st_release_sys(reinterpret_cast<int32_t*>(flags_ptrs[d]) + world + me, epoch);
   for (int d = threadIdx.x; d < world; d += blockDim.x) {
     if (d == me || count[d] <= 0) continue;
-    int32_t* f = reinterpret_cast<int32_t*>(flags_ptrs[d]) + me;
-    asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+    const int32_t* f = reinterpret_cast<const int32_t*>(flags_ptrs[me]) + world + d;
+    while (ld_acquire_sys(f) < epoch) {
+    }
   }
+}
+
+// Exit handshake: publish "done" to every rank we stored into, then wait for
+// "done" from every rank that stores into us.
+__global__ void remap_done_kernel(const int64_t* __restrict__ flags_ptrs,
+                                  const int32_t* __restrict__ count,
+                                  const int32_t* __restrict__ expect, int world, int me,
+                                  int32_t epoch) {
+  __threadfence_system();
+  for (int d = threadIdx.x; d < world; d += blockDim.x)
+    if (d != me && count[d] > 0) st_release_sys(reinterpret_cast<int32_t*>(flags_ptrs[d]) + me, epoch);
   for (int s = threadIdx.x; s < world; s += blockDim.x) {
     if (s == me || expect[s] == 0) continue;
     const int32_t* f = reinterpret_cast<const int32_t*>(flags_ptrs[me]) + s;
-    int32_t v;
-    do {
-      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-    } while (v < epoch);
+    while (ld_acquire_sys(f) < epoch) {
+    }
   }
 }
 
@@ -139,6 +162,9 @@ extern "C" int zp_remap_push(const void* src, int64_t row_bytes, const int64_t* 
     return zp_fail(ZP_EINVAL, "zp_remap_push: null table");
   if (zp_check_device() != ZP_OK) return ZP_ENODEV;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  zp::remap_ready_kernel<<<1, 64, 0, st>>>(flags_ptrs, count, world, my_rank, epoch);
+  cudaError_t e0 = cudaGetLastError();
+  if (e0 != cudaSuccess) return zp_fail_cuda(e0, "zp_remap_push: ready launch");
   if (max_count > 0) {
     dim3 grid(grid_for(int64_t(max_count) * (row_bytes / 16), world), world);
     zp::remap_push_kernel<<<grid, zp::kMoveThreads, 0, st>>>(
@@ -146,7 +172,7 @@ extern "C" int zp_remap_push(const void* src, int64_t row_bytes, const int64_t* 
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_push: launch");
   }
-  zp::remap_signal_kernel<<<1, 64, 0, st>>>(flags_ptrs, count, expect, world, my_rank, epoch);
+  zp::remap_done_kernel<<<1, 64, 0, st>>>(flags_ptrs, count, expect, world, my_rank, epoch);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_push: signal launch");
   return ZP_OK;

@@ -242,6 +242,112 @@ def remap_inverse(layout: RemapLayout, y: torch.Tensor, ctx: RankContext | None 
     return x
 
 
+# ------------------------------------------------------------------ fused remap (peer stores)
+
+_opened: dict[bytes, int] = {}
+
+
+def _ipc_export(t: torch.Tensor) -> tuple[bytes, int]:
+    """CUDA-IPC handle of the allocation holding ``t`` plus t's byte offset in it."""
+    info = t.untyped_storage()._share_cuda_()
+    handle, storage_offset = info[1], info[3]
+    return bytes(handle), int(storage_offset) + t.storage_offset() * t.element_size()
+
+
+def _ipc_open(handle: bytes, offset: int) -> int:
+    base = _opened.get(handle)
+    if base is None:
+        import ctypes
+        out = ctypes.c_void_p()
+        from . import _native
+        buf = ctypes.create_string_buffer(handle, 64)
+        _native.check(_native.lib().zp_ipc_open_handle(buf, ctypes.byref(out)), "zp_ipc_open_handle")
+        base = int(out.value)
+        _opened[handle] = base
+    return base + offset
+
+
+class PeerBuffer:
+    """A landing buffer every rank can store into over NVLink (CUDA IPC), with
+    its int32[2*world] ready/done flag block.  Collective constructor."""
+
+    def __init__(self, ctx: RankContext, rows: int, row_elems: int, dtype=torch.bfloat16):
+        self.ctx = ctx
+        self.buf = torch.empty(max(rows, 1), row_elems, dtype=dtype, device=ctx.device)
+        self.flags = torch.zeros(2 * ctx.world, dtype=torch.int32, device=ctx.device)
+        torch.cuda.synchronize(ctx.device)
+        mine = (_ipc_export(self.buf), _ipc_export(self.flags))
+        everyone = [None] * ctx.world
+        dist.all_gather_object(everyone, mine, group=ctx.group)
+        ptrs, fptrs = [], []
+        for r, ((bh, bo), (fh, fo)) in enumerate(everyone):
+            if r == ctx.rank:
+                ptrs.append(self.buf.data_ptr())
+                fptrs.append(self.flags.data_ptr())
+            else:
+                ptrs.append(_ipc_open(bh, bo))
+                fptrs.append(_ipc_open(fh, fo))
+        self.peer_ptrs = torch.tensor(ptrs, dtype=torch.int64, device=ctx.device)
+        self.flag_ptrs = torch.tensor(fptrs, dtype=torch.int64, device=ctx.device)
+        self.epoch = 0
+        dist.barrier(group=ctx.group)
+
+    @property
+    def row_bytes(self) -> int:
+        return self.buf.shape[1] * self.buf.element_size()
+
+
+@dataclass
+class _PushTables:
+    table: torch.Tensor  # int32 [4, world]: src_row0, dst_row0, count, expect
+    max_count: int
+
+
+def push_tables(layout: RemapLayout, rank: int, inverse: bool, device) -> _PushTables:
+    """Per-destination rows for zp_remap_push (forward: attention -> linear)."""
+    w = layout.world
+    m = layout.matrix
+    if not inverse:
+        count = [int(m[rank, d]) for d in range(w)]
+        src0 = layout.send_offsets(rank)
+        dst0 = [layout.recv_offsets(d)[rank] for d in range(w)]
+        expect = [int(m[s, rank] > 0) for s in range(w)]
+    else:
+        count = [int(m[d, rank]) for d in range(w)]
+        src0 = layout.recv_offsets(rank)
+        dst0 = [layout.send_offsets(d)[rank] for d in range(w)]
+        expect = [int(m[rank, s] > 0) for s in range(w)]
+    host = torch.tensor([src0, dst0, count, expect], dtype=torch.int32)
+    return _PushTables(host.pin_memory().to(device, non_blocking=True), max(count) if count else 0)
+
+
+def remap_push(layout: RemapLayout, x: torch.Tensor, peer: PeerBuffer, ctx: RankContext,
+               inverse: bool = False, tables: _PushTables | None = None) -> torch.Tensor:
+    """Fused remap: this rank's outgoing rows are stored straight into the
+    receivers' ``peer`` buffers (one kernel, NVLink peer stores, ready/done
+    epoch flags) — the all-to-allv without a collective library.  Kept rows
+    are copied only if ``x`` is not already ``peer.buf``'s prefix.  Returns the
+    local landing view (linear layout for forward, attention layout for
+    inverse)."""
+    from . import _native
+    r = ctx.rank
+    a, b = layout.attn_rows[r], layout.linear_rows[r]
+    rows_in, rows_out = (b, a) if inverse else (a, b)
+    if x.shape[0] != rows_in:
+        raise ValueError(f"rank {r}: remap input has {x.shape[0]} rows, layout says {rows_in}")
+    out = peer.buf[:rows_out]
+    _copy_prefix(out, x, min(a, b), ctx)
+    tb = tables or push_tables(layout, r, inverse, x.device)
+    peer.epoch += 1
+    t = tb.table
+    ops._count_launch(3)
+    _native.call("zp_remap_push", x.data_ptr(), peer.row_bytes, peer.peer_ptrs.data_ptr(),
+                 t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), peer.flag_ptrs.data_ptr(),
+                 t[3].data_ptr(), ctx.world, r, peer.epoch, tb.max_count,
+                 int(torch.cuda.current_stream().cuda_stream))
+    return out
+
+
 # ------------------------------------------------------------------ layer
 
 class ZeppelinLayer:

@@ -33,6 +33,11 @@ def launch_count() -> int:
     return _launches
 
 
+def _count_launch(n: int = 1) -> None:
+    global _launches
+    _launches += n
+
+
 def set_launch_hook(fn) -> None:
     global _hook
     _hook = fn

@@ -48,6 +48,19 @@ def _worker(rank, world, port, lengths, results):
         ids = torch.cat([ids, torch.zeros(q.shape[0], 2, dtype=torch.int32)], 1).cuda()  # 16-byte rows
         y = engine.remap_forward(lay, ids, ctx)
         back = engine.remap_inverse(lay, y, ctx)
+        # fused peer-store path (CUDA IPC landing buffers), twice to exercise epochs
+        lin = engine.PeerBuffer(ctx, max(lay.linear_rows), 4, torch.int32)
+        att = engine.PeerBuffer(ctx, max(lay.attn_rows), 4, torch.int32)
+        push_ok = True
+        for it in range(2):
+            att.buf[:q.shape[0]].copy_(ids)
+            yp = engine.remap_push(lay, att.buf[:q.shape[0]], lin, ctx)
+            torch.cuda.synchronize()
+            push_ok &= bool(torch.equal(yp, y))
+            yp[:, 2] = it + 7  # scribble, then bring the rows home
+            bp = engine.remap_push(lay, yp, att, ctx, inverse=True)
+            torch.cuda.synchronize()
+            push_ok &= bool(torch.equal(bp[:, :2], ids[:, :2])) and bool((bp[:, 2] == it + 7).all())
         torch.cuda.synchronize()
         f64 = lambda m: {s: t.double().numpy() for s, t in m.items()}  # noqa: E731
         ref, _ = OA.run_plan(plan, sched, f64(sq), f64(sk), f64(sv), 128 ** -0.5)
@@ -55,7 +68,7 @@ def _worker(rank, world, port, lengths, results):
         want = OR.source_map(list(lay.attn_rows), lay.matrix)[rank]
         perm_ok = bool(np.array_equal(y[:, :2].cpu().numpy(), want))
         back_ok = bool(torch.equal(back, ids))
-        results[rank] = (err, perm_ok, back_ok, len(plan.ring_groups))
+        results[rank] = (err, perm_ok, back_ok and push_ok, len(plan.ring_groups))
     finally:
         dist.destroy_process_group()
 
