@@ -119,8 +119,10 @@ ZP_API int zp_remap_push(const void* src, int64_t row_bytes, const int64_t* dst_
                   const int64_t* flags_ptrs, const int32_t* expect, int world, int my_rank,
                   int32_t epoch, int max_count, void* stream);
 
-/* CUDA IPC helpers for zp_remap_push (host pointers to 64-byte handles). */
-ZP_API int zp_ipc_get_handle(void* dev_ptr, void* handle_out64);
+/* CUDA IPC helpers for zp_remap_push (host pointers to 64-byte handles).
+ * get_handle exports the allocation containing dev_ptr and returns dev_ptr's
+ * byte offset inside it; a peer maps it with open_handle and adds the offset. */
+ZP_API int zp_ipc_get_handle(void* dev_ptr, void* handle_out64, int64_t* offset_out);
 ZP_API int zp_ipc_open_handle(const void* handle64, void** dev_ptr_out);
 ZP_API int zp_ipc_close_handle(void* dev_ptr);
 

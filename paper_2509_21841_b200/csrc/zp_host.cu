@@ -90,11 +90,28 @@ extern "C" int zp_device_sm_count(void) {
   return n;
 }
 
-extern "C" int zp_ipc_get_handle(void* dev_ptr, void* handle_out64) {
+extern "C" int zp_ipc_get_handle(void* dev_ptr, void* handle_out64, int64_t* offset_out) {
+  typedef CUresult (*PFN_range)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static PFN_range range_fn = nullptr;
+  if (!range_fn) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      cudaGetLastError();
+      return zp_fail(ZP_ENODEV, "cuMemGetAddressRange entry point unavailable");
+    }
+    range_fn = reinterpret_cast<PFN_range>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range_fn(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return zp_fail(ZP_ECUDA, "cuMemGetAddressRange failed");
   cudaIpcMemHandle_t h;
-  cudaError_t e = cudaIpcGetMemHandle(&h, dev_ptr);
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
   if (e != cudaSuccess) return zp_fail_cuda(e, "cudaIpcGetMemHandle");
   std::memcpy(handle_out64, &h, sizeof(h));
+  *offset_out = int64_t(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
   return ZP_OK;
 }
 

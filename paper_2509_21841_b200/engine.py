@@ -249,9 +249,12 @@ _opened: dict[bytes, int] = {}
 
 def _ipc_export(t: torch.Tensor) -> tuple[bytes, int]:
     """CUDA-IPC handle of the allocation holding ``t`` plus t's byte offset in it."""
-    info = t.untyped_storage()._share_cuda_()
-    handle, storage_offset = info[1], info[3]
-    return bytes(handle), int(storage_offset) + t.storage_offset() * t.element_size()
+    import ctypes
+    from . import _native
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64()
+    _native.check(_native.lib().zp_ipc_get_handle(t.data_ptr(), h, ctypes.byref(off)), "zp_ipc_get_handle")
+    return h.raw, int(off.value)
 
 
 def _ipc_open(handle: bytes, offset: int) -> int:
