@@ -155,7 +155,13 @@ def run_gpu(args):
     # its prefix [0, A_r), the linear layout its prefix [0, B_r); kept rows
     # never move, only the remapped tail crosses NVLink.
     lin_rows = max(lay.linear_rows[rank], rows, 1)
-    act = torch.empty(lin_rows, hq * d, device=dev, dtype=torch.bfloat16)
+    if world > 1:
+        # IPC-shared so peers can read their incoming rows straight out of it
+        peer = engine.PeerBuffer(ctx, cluster.token_capacity, hq * d)
+        act = peer.buf
+    else:
+        peer = None
+        act = torch.empty(lin_rows, hq * d, device=dev, dtype=torch.bfloat16)
     o = act[:rows].view(rows, hq, d)
     lse = torch.empty(hq, max(rows, 1), device=dev)
 
@@ -167,8 +173,13 @@ def run_gpu(args):
             ops.set_launch_hook(lambda name, a, b: attn_events.append((name, a, b)))
         engine.attention_forward(plan_, sched_, q, k, v, ctx, prog_, devp_, out=(o, lse))
         ops.set_launch_hook(None)
-        yy = engine.remap_forward(prog_.remap, act[:rows], ctx, out=act[:prog_.remap.linear_rows[rank]])
-        engine.remap_inverse(prog_.remap, yy, ctx, out=act[:rows])
+        if peer is not None:
+            # fused remap kernel: peer loads over NVLink, in place
+            engine.remap_pull(prog_.remap, peer, act, ctx)
+            engine.remap_pull(prog_.remap, peer, act, ctx, inverse=True)
+        else:
+            yy = engine.remap_forward(prog_.remap, act[:rows], ctx, out=act[:prog_.remap.linear_rows[rank]])
+            engine.remap_inverse(prog_.remap, yy, ctx, out=act[:rows])
 
     for _ in range(args.warmup):
         step()
@@ -365,14 +376,23 @@ def run_remap_stress(ctx, dev, world, rank, args, total=262144, iters=10):
         sent = [int(lay.matrix[i].sum()) * hidden * 2 for i in range(world)]
         busiest = max(sent)
         res = {"counts": counts, "rows_moved": lay.moved_rows(), "busiest_sender_bytes": busiest}
-        att = engine.PeerBuffer(ctx, max(lay.attn_rows), hidden)
-        lin = engine.PeerBuffer(ctx, max(lay.linear_rows), hidden)
-        att.buf.normal_()
-        x = att.buf[:a]
+        # one IPC-shared activation buffer per rank with max(A_i, B_i) rows:
+        # the attention layout is its prefix [0, A_i), the linear layout its
+        # prefix [0, B_i); kept rows never move, only remapped rows cross NVLink
+        act = engine.PeerBuffer(ctx, max(max(lay.attn_rows), max(lay.linear_rows)), hidden)
+        act.buf.normal_()
+        x, yv = act.buf[:a], act.buf[:b]
         tabs = engine.push_tables(lay, rank, False, dev)
+        ptabs = engine.pull_tables(lay, rank, False, dev)
+        lay0 = remap_layout([1] * world)  # nothing moves: ready + done kernels only
+        tabs0 = engine.push_tables(lay0, rank, False, dev)
         paths = {
-            "nccl_all_to_allv": lambda: engine.remap_forward(lay, x, ctx, out=lin.buf[:b]),
-            "fused_peer_store": lambda: engine.remap_push(lay, x, lin, ctx, tables=tabs),
+            "nccl_all_to_allv": lambda: engine.remap_forward(lay, x, ctx, out=yv),
+            "fused_peer_store": lambda: engine.remap_push(lay, x, act, ctx, tables=tabs),
+            "fused_peer_load": lambda: engine.remap_pull(lay, act, act.buf, ctx, tables=ptabs),
+            "copy_engine_push": lambda: engine.remap_push(lay, x, act, ctx, tables=tabs, copy_engine=True),
+            "copy_engine_pull": lambda: engine.remap_pull(lay, act, act.buf, ctx, tables=ptabs, copy_engine=True),
+            "handshake_only": lambda: engine.remap_push(lay0, act.buf[:1], act, ctx, tables=tabs0),
         }
         for pname, fn in paths.items():
             for _ in range(3):
@@ -391,16 +411,24 @@ def run_remap_stress(ctx, dev, world, rank, args, total=262144, iters=10):
             gbs = busiest / (ms / 1e3) / 1e9
             res[pname] = {"ms": ms, "GB_per_s_busiest_sender": gbs, "frac_nvlink_900": gbs / 900.0,
                           "frac_nvlink_770_measured": gbs / 770.0}
-        # exactness of the fused path against the NCCL path on these rows
-        y1 = engine.remap_forward(lay, x, ctx).clone()
-        y2 = engine.remap_push(lay, x, lin, ctx, tables=tabs)
-        torch.cuda.synchronize()
-        ok = torch.tensor([int(torch.equal(y1, y2))], device=dev)
+        # exactness: every path lands the same rows (rows are overwritten with
+        # the same payload each time, the sources never change)
+        ref = torch.empty_like(act.buf)
+        ref[:b] = engine.remap_forward(lay, x.clone(), ctx)
+        same = True
+        for pname, fn in paths.items():
+            if pname == "handshake_only":
+                continue
+            act.buf[a:].zero_() if b > a else None
+            fn()
+            torch.cuda.synchronize()
+            same &= bool(torch.equal(act.buf[:b], ref[:b]))
+        ok = torch.tensor([int(same)], device=dev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        res["fused_equals_nccl"] = bool(ok.item())
-        out[name] = res
-        del att, lin
+        res["all_paths_equal"] = bool(ok.item())
+        del act, ref
         torch.cuda.empty_cache()
+        out[name] = res
     return out
 
 

@@ -119,6 +119,39 @@ ZP_API int zp_remap_push(const void* src, int64_t row_bytes, const int64_t* dst_
                   const int64_t* flags_ptrs, const int32_t* expect, int world, int my_rank,
                   int32_t epoch, int max_count, void* stream);
 
+/* Fused remap, pull form (collective): rank `my_rank` copies rows
+ * [src_row0[s], +count[s]) of source rank s's buffer src_ptrs[s] (peer
+ * pointer) into its local `dst` at row dst_row0[s] — peer LDG.128 over
+ * NVLink.  Handshake as zp_remap_push with the roles of the flags swapped:
+ * ready = "my rows are final for `epoch`", done = "I finished reading your
+ * rows"; the call returns (on `stream`) only after every rank with
+ * readers[r] != 0 has read this rank's rows. */
+ZP_API int zp_remap_pull(void* dst, int64_t row_bytes, const int64_t* src_ptrs,
+                  const int32_t* src_row0, const int32_t* dst_row0, const int32_t* count,
+                  const int64_t* flags_ptrs, const int32_t* readers, int world, int my_rank,
+                  int32_t epoch, int max_count, void* stream);
+
+/* Same contract as zp_remap_pull, but the row blocks are moved by the copy
+ * engines (one cudaMemcpyAsync per source rank, enqueued between the ready
+ * and done handshake kernels), leaving every SM free for concurrent compute.
+ * Row tables are HOST arrays here; count_dev / readers_dev are their device
+ * copies for the handshake kernels. */
+ZP_API int zp_remap_pull_ce(void* dst, int64_t row_bytes, const int64_t* src_ptrs_host,
+                     const int32_t* src_row0_host, const int32_t* dst_row0_host,
+                     const int32_t* count_host, const int64_t* flags_ptrs,
+                     const int32_t* count_dev, const int32_t* readers_dev, int world,
+                     int my_rank, int32_t epoch, void* stream);
+
+/* zp_remap_push with the row blocks written by the sender's copy engines
+ * (one cudaMemcpyAsync per destination into its IPC-mapped buffer) between
+ * the ready and done handshake kernels.  Host row tables + device copies of
+ * count / expect for the handshake. */
+ZP_API int zp_remap_push_ce(const void* src, int64_t row_bytes, const int64_t* dst_ptrs_host,
+                     const int32_t* src_row0_host, const int32_t* dst_row0_host,
+                     const int32_t* count_host, const int64_t* flags_ptrs,
+                     const int32_t* count_dev, const int32_t* expect_dev, int world,
+                     int my_rank, int32_t epoch, void* stream);
+
 /* CUDA IPC helpers for zp_remap_push (host pointers to 64-byte handles).
  * get_handle exports the allocation containing dev_ptr and returns dev_ptr's
  * byte offset inside it; a peer maps it with open_handle and adds the offset. */

@@ -28,6 +28,12 @@ SIGNATURES: dict[str, tuple] = {
     "zp_copy_rows": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_i64, _vp, _c_int, _c_int, _vp]),
     "zp_remap_push": (_c_int, [_vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                ctypes.c_int32, _c_int, _vp]),
+    "zp_remap_pull": (_c_int, [_vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
+                               ctypes.c_int32, _c_int, _vp]),
+    "zp_remap_pull_ce": (_c_int, [_vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
+                                  ctypes.c_int32, _vp]),
+    "zp_remap_push_ce": (_c_int, [_vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
+                                  ctypes.c_int32, _vp]),
     "zp_ipc_get_handle": (_c_int, [_vp, _vp, ctypes.POINTER(_c_i64)]),
     "zp_ipc_open_handle": (_c_int, [_vp, ctypes.POINTER(_vp)]),
     "zp_ipc_close_handle": (_c_int, [_vp]),

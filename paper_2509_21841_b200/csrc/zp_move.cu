@@ -10,7 +10,29 @@
 #include "zp_host.h"
 #include "../../include/zeppelin_b200.h"
 
+#ifndef ZP_PUSH_BULK
+#define ZP_PUSH_BULK 0
+#endif
+
 namespace zp {
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init_raw(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_raw(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
 
 constexpr int kMoveThreads = 256;
 constexpr int kUnroll = 4;
@@ -73,6 +95,108 @@ __global__ void __launch_bounds__(kMoveThreads)
   }
   for (; i < total; i += step) t[i] = __ldg(s + i);
   __threadfence_system();
+}
+
+// TMA bulk-copy variant of the push: one elected thread per CTA streams its
+// share of the destination's rows HBM -> SMEM (cp.async.bulk, mbarrier) ->
+// peer HBM (cp.async.bulk.global.shared::cta, bulk groups), kStages deep, so
+// the copy engine path, not SM load/store issue, moves the bytes over NVLink.
+constexpr int kBulkStages = 4;
+constexpr uint32_t kBulkChunk = 32768;
+
+__global__ void __launch_bounds__(32)
+    remap_push_bulk_kernel(const uint8_t* __restrict__ src, int64_t row_bytes,
+                           const int64_t* __restrict__ dst_ptrs, const int32_t* __restrict__ src_row0,
+                           const int32_t* __restrict__ dst_row0, const int32_t* __restrict__ count) {
+  extern __shared__ __align__(128) uint8_t bulk_smem[];
+  __shared__ __align__(8) uint64_t full[kBulkStages];
+  const int d = blockIdx.y;
+  const int64_t n = count[d];
+  if (n <= 0 || threadIdx.x != 0) return;
+  const int64_t bytes = n * row_bytes;
+  const uint8_t* s = src + int64_t(src_row0[d]) * row_bytes;
+  uint8_t* t = reinterpret_cast<uint8_t*>(dst_ptrs[d]) + int64_t(dst_row0[d]) * row_bytes;
+  // contiguous byte range of this CTA (16-byte aligned split)
+  const int64_t per = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~int64_t(15);
+  const int64_t lo = min(bytes, per * int64_t(blockIdx.x));
+  const int64_t hi = min(bytes, lo + per);
+  if (lo >= hi) return;
+  for (int i = 0; i < kBulkStages; ++i) mbar_init_raw(smem_addr(&full[i]), 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const int64_t nchunks = (hi - lo + kBulkChunk - 1) / kBulkChunk;
+  auto load = [&](int64_t c) {
+    const int st = int(c % kBulkStages);
+    const int64_t off = lo + c * kBulkChunk;
+    const uint32_t len = uint32_t(((hi - off) < int64_t(kBulkChunk) ? (hi - off) : int64_t(kBulkChunk)));
+    const uint32_t bar = smem_addr(&full[st]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(len) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(bulk_smem + st * kBulkChunk)),
+        "l"(s + off), "r"(len), "r"(bar)
+        : "memory");
+  };
+  for (int64_t c = 0; c < (nchunks < kBulkStages ? nchunks : int64_t(kBulkStages)); ++c) load(c);
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int st = int(c % kBulkStages);
+    const int64_t off = lo + c * kBulkChunk;
+    const uint32_t len = uint32_t(((hi - off) < int64_t(kBulkChunk) ? (hi - off) : int64_t(kBulkChunk)));
+    mbar_wait_raw(smem_addr(&full[st]), uint32_t(c / kBulkStages) & 1);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(t + off),
+                 "r"(smem_addr(bulk_smem + st * kBulkChunk)), "r"(len)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    if (c + kBulkStages < nchunks) {
+      // the stage is reloaded only after its store has finished reading SMEM
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      load(c + kBulkStages);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  __threadfence_system();
+}
+
+// Pull variant: the receiver reads its incoming rows straight out of the
+// senders' buffers over NVLink (peer LDG.128, L1 no-allocate) and writes them
+// locally.  grid.y = source rank.
+__device__ __forceinline__ uint4 ld_peer(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+#ifndef ZP_PULL_UNROLL
+#define ZP_PULL_UNROLL 8
+#endif
+// Each CTA copies one contiguous span of the source's rows: a warp's U loads
+// cover U*512 consecutive bytes, keeping the remote DRAM access sequential.
+__global__ void __launch_bounds__(kMoveThreads)
+    remap_pull_kernel(uint8_t* __restrict__ dst, int64_t row_bytes, const int64_t* __restrict__ src_ptrs,
+                      const int32_t* __restrict__ src_row0, const int32_t* __restrict__ dst_row0,
+                      const int32_t* __restrict__ count) {
+  constexpr int U = ZP_PULL_UNROLL;
+  constexpr int64_t kSpan = int64_t(kMoveThreads) * U;  // vectors per CTA iteration
+  const int sr = blockIdx.y;
+  const int n = count[sr];
+  if (n <= 0) return;
+  const int64_t row_vecs = row_bytes / 16;
+  const uint4* s = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(src_ptrs[sr]) +
+                                                  int64_t(src_row0[sr]) * row_bytes);
+  uint4* t = reinterpret_cast<uint4*>(dst + int64_t(dst_row0[sr]) * row_bytes);
+  const int64_t total = int64_t(n) * row_vecs;
+  for (int64_t base = int64_t(blockIdx.x) * kSpan; base < total; base += int64_t(gridDim.x) * kSpan) {
+    if (base + kSpan <= total) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld_peer(s + base + u * kMoveThreads + threadIdx.x);
+#pragma unroll
+      for (int u = 0; u < U; ++u) t[base + u * kMoveThreads + threadIdx.x] = v[u];
+    } else {
+      for (int64_t i = base + threadIdx.x; i < total; i += kMoveThreads) t[i] = ld_peer(s + i);
+    }
+  }
 }
 
 // Flag layout per rank (int32[2*world], IPC-shared): [0, world) "done" —
@@ -166,14 +290,116 @@ extern "C" int zp_remap_push(const void* src, int64_t row_bytes, const int64_t* 
   cudaError_t e0 = cudaGetLastError();
   if (e0 != cudaSuccess) return zp_fail_cuda(e0, "zp_remap_push: ready launch");
   if (max_count > 0) {
+#if ZP_PUSH_BULK
+    static bool attr = false;
+    const int smem = zp::kBulkStages * int(zp::kBulkChunk);
+    if (!attr) {
+      cudaFuncSetAttribute(zp::remap_push_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr = true;
+    }
+    const int64_t bytes = int64_t(max_count) * row_bytes;
+    int per_dest = int((bytes + (1 << 20) - 1) >> 20);  // ~1 MB per CTA
+    const int cap = 2 * 148 / world + 1;
+    per_dest = per_dest < 1 ? 1 : (per_dest > cap ? cap : per_dest);
+    zp::remap_push_bulk_kernel<<<dim3(per_dest, world), 32, smem, st>>>(
+        reinterpret_cast<const uint8_t*>(src), row_bytes, dst_ptrs, src_row0, dst_row0, count);
+#else
     dim3 grid(grid_for(int64_t(max_count) * (row_bytes / 16), world), world);
     zp::remap_push_kernel<<<grid, zp::kMoveThreads, 0, st>>>(
         reinterpret_cast<const uint8_t*>(src), row_bytes, dst_ptrs, src_row0, dst_row0, count);
+#endif
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_push: launch");
   }
   zp::remap_done_kernel<<<1, 64, 0, st>>>(flags_ptrs, count, expect, world, my_rank, epoch);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_push: signal launch");
+  return ZP_OK;
+}
+
+extern "C" int zp_remap_pull(void* dst, int64_t row_bytes, const int64_t* src_ptrs,
+                             const int32_t* src_row0, const int32_t* dst_row0, const int32_t* count,
+                             const int64_t* flags_ptrs, const int32_t* readers, int world,
+                             int my_rank, int32_t epoch, int max_count, void* stream) {
+  if (world < 1 || world > 64 || my_rank < 0 || my_rank >= world || max_count < 0)
+    return zp_fail(ZP_EINVAL, "zp_remap_pull: bad world/rank");
+  if ((reinterpret_cast<uintptr_t>(dst) & 15u) || (row_bytes & 15) || row_bytes <= 0)
+    return zp_fail(ZP_EINVAL, "zp_remap_pull: dst and row bytes must be 16-byte aligned");
+  if (!src_ptrs || !src_row0 || !dst_row0 || !count || !flags_ptrs || !readers)
+    return zp_fail(ZP_EINVAL, "zp_remap_pull: null table");
+  if (zp_check_device() != ZP_OK) return ZP_ENODEV;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // ready: my source rows are final for this epoch; wait for my sources (count > 0)
+  zp::remap_ready_kernel<<<1, 64, 0, st>>>(flags_ptrs, count, world, my_rank, epoch);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_pull: ready launch");
+  if (max_count > 0) {
+    dim3 grid(grid_for(int64_t(max_count) * (row_bytes / 16), world), world);
+    zp::remap_pull_kernel<<<grid, zp::kMoveThreads, 0, st>>>(reinterpret_cast<uint8_t*>(dst), row_bytes,
+                                                             src_ptrs, src_row0, dst_row0, count);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_pull: launch");
+  }
+  // done: tell each source I finished reading it; wait until every reader of my
+  // rows finished, so the caller may overwrite them
+  zp::remap_done_kernel<<<1, 64, 0, st>>>(flags_ptrs, count, readers, world, my_rank, epoch);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_pull: done launch");
+  return ZP_OK;
+}
+
+extern "C" int zp_remap_pull_ce(void* dst, int64_t row_bytes, const int64_t* src_ptrs_host,
+                                const int32_t* src_row0_host, const int32_t* dst_row0_host,
+                                const int32_t* count_host, const int64_t* flags_ptrs,
+                                const int32_t* count_dev, const int32_t* readers_dev, int world,
+                                int my_rank, int32_t epoch, void* stream) {
+  if (world < 1 || world > 64 || my_rank < 0 || my_rank >= world)
+    return zp_fail(ZP_EINVAL, "zp_remap_pull_ce: bad world/rank");
+  if (!src_ptrs_host || !src_row0_host || !dst_row0_host || !count_host || !flags_ptrs ||
+      !count_dev || !readers_dev)
+    return zp_fail(ZP_EINVAL, "zp_remap_pull_ce: null table");
+  if (zp_check_device() != ZP_OK) return ZP_ENODEV;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  zp::remap_ready_kernel<<<1, 64, 0, st>>>(flags_ptrs, count_dev, world, my_rank, epoch);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_pull_ce: ready launch");
+  for (int s = 0; s < world; ++s) {
+    if (count_host[s] <= 0) continue;
+    e = cudaMemcpyAsync(reinterpret_cast<uint8_t*>(dst) + int64_t(dst_row0_host[s]) * row_bytes,
+                        reinterpret_cast<const uint8_t*>(src_ptrs_host[s]) + int64_t(src_row0_host[s]) * row_bytes,
+                        size_t(count_host[s]) * size_t(row_bytes), cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_pull_ce: copy");
+  }
+  zp::remap_done_kernel<<<1, 64, 0, st>>>(flags_ptrs, count_dev, readers_dev, world, my_rank, epoch);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_pull_ce: done launch");
+  return ZP_OK;
+}
+
+extern "C" int zp_remap_push_ce(const void* src, int64_t row_bytes, const int64_t* dst_ptrs_host,
+                                const int32_t* src_row0_host, const int32_t* dst_row0_host,
+                                const int32_t* count_host, const int64_t* flags_ptrs,
+                                const int32_t* count_dev, const int32_t* expect_dev, int world,
+                                int my_rank, int32_t epoch, void* stream) {
+  if (world < 1 || world > 64 || my_rank < 0 || my_rank >= world)
+    return zp_fail(ZP_EINVAL, "zp_remap_push_ce: bad world/rank");
+  if (!dst_ptrs_host || !src_row0_host || !dst_row0_host || !count_host || !flags_ptrs ||
+      !count_dev || !expect_dev)
+    return zp_fail(ZP_EINVAL, "zp_remap_push_ce: null table");
+  if (zp_check_device() != ZP_OK) return ZP_ENODEV;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  zp::remap_ready_kernel<<<1, 64, 0, st>>>(flags_ptrs, count_dev, world, my_rank, epoch);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_push_ce: ready launch");
+  for (int d = 0; d < world; ++d) {
+    if (count_host[d] <= 0) continue;
+    e = cudaMemcpyAsync(reinterpret_cast<uint8_t*>(dst_ptrs_host[d]) + int64_t(dst_row0_host[d]) * row_bytes,
+                        reinterpret_cast<const uint8_t*>(src) + int64_t(src_row0_host[d]) * row_bytes,
+                        size_t(count_host[d]) * size_t(row_bytes), cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_push_ce: copy");
+  }
+  zp::remap_done_kernel<<<1, 64, 0, st>>>(flags_ptrs, count_dev, expect_dev, world, my_rank, epoch);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_push_ce: done launch");
   return ZP_OK;
 }

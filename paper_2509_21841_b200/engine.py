@@ -293,6 +293,7 @@ class PeerBuffer:
         self.peer_ptrs = torch.tensor(ptrs, dtype=torch.int64, device=ctx.device)
         self.flag_ptrs = torch.tensor(fptrs, dtype=torch.int64, device=ctx.device)
         self.epoch = 0
+        self.host_ptrs = None
         dist.barrier(group=ctx.group)
 
     @property
@@ -302,8 +303,9 @@ class PeerBuffer:
 
 @dataclass
 class _PushTables:
-    table: torch.Tensor  # int32 [4, world]: src_row0, dst_row0, count, expect
+    table: torch.Tensor  # int32 [4, world]: src_row0, dst_row0, count, expect/readers
     max_count: int
+    host: np.ndarray | None = None  # same table on the host (copy-engine path)
 
 
 def push_tables(layout: RemapLayout, rank: int, inverse: bool, device) -> _PushTables:
@@ -321,11 +323,13 @@ def push_tables(layout: RemapLayout, rank: int, inverse: bool, device) -> _PushT
         dst0 = [layout.send_offsets(d)[rank] for d in range(w)]
         expect = [int(m[rank, s] > 0) for s in range(w)]
     host = torch.tensor([src0, dst0, count, expect], dtype=torch.int32)
-    return _PushTables(host.pin_memory().to(device, non_blocking=True), max(count) if count else 0)
+    return _PushTables(host.pin_memory().to(device, non_blocking=True), max(count) if count else 0,
+                       np.ascontiguousarray(host.numpy()))
 
 
 def remap_push(layout: RemapLayout, x: torch.Tensor, peer: PeerBuffer, ctx: RankContext,
-               inverse: bool = False, tables: _PushTables | None = None) -> torch.Tensor:
+               inverse: bool = False, tables: _PushTables | None = None,
+               copy_engine: bool = False) -> torch.Tensor:
     """Fused remap: this rank's outgoing rows are stored straight into the
     receivers' ``peer`` buffers (one kernel, NVLink peer stores, ready/done
     epoch flags) — the all-to-allv without a collective library.  Kept rows
@@ -343,12 +347,76 @@ def remap_push(layout: RemapLayout, x: torch.Tensor, peer: PeerBuffer, ctx: Rank
     tb = tables or push_tables(layout, r, inverse, x.device)
     peer.epoch += 1
     t = tb.table
+    if copy_engine:
+        if peer.host_ptrs is None:
+            peer.host_ptrs = np.ascontiguousarray(peer.peer_ptrs.cpu().numpy())
+        h = tb.host
+        ops._count_launch(2)
+        _native.call("zp_remap_push_ce", x.data_ptr(), peer.row_bytes, peer.host_ptrs.ctypes.data,
+                     h[0].ctypes.data, h[1].ctypes.data, h[2].ctypes.data, peer.flag_ptrs.data_ptr(),
+                     t[2].data_ptr(), t[3].data_ptr(), ctx.world, r, peer.epoch,
+                     int(torch.cuda.current_stream().cuda_stream))
+        return out
     ops._count_launch(3)
     _native.call("zp_remap_push", x.data_ptr(), peer.row_bytes, peer.peer_ptrs.data_ptr(),
                  t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), peer.flag_ptrs.data_ptr(),
                  t[3].data_ptr(), ctx.world, r, peer.epoch, tb.max_count,
                  int(torch.cuda.current_stream().cuda_stream))
     return out
+
+
+def pull_tables(layout: RemapLayout, rank: int, inverse: bool, device) -> _PushTables:
+    """Per-source rows for zp_remap_pull (forward: attention -> linear)."""
+    w = layout.world
+    m = layout.matrix
+    if not inverse:
+        count = [int(m[s, rank]) for s in range(w)]
+        src0 = [layout.send_offsets(s)[rank] for s in range(w)]
+        dst0 = layout.recv_offsets(rank)
+        readers = [int(m[rank, d] > 0) for d in range(w)]
+    else:
+        count = [int(m[rank, d]) for d in range(w)]
+        src0 = [layout.recv_offsets(d)[rank] for d in range(w)]
+        dst0 = layout.send_offsets(rank)
+        readers = [int(m[s, rank] > 0) for s in range(w)]
+    host = torch.tensor([src0, dst0, count, readers], dtype=torch.int32)
+    return _PushTables(host.pin_memory().to(device, non_blocking=True), max(count) if count else 0,
+                       np.ascontiguousarray(host.numpy()))
+
+
+def remap_pull(layout: RemapLayout, src: PeerBuffer, out: torch.Tensor, ctx: RankContext,
+               inverse: bool = False, tables: _PushTables | None = None,
+               copy_engine: bool = False) -> torch.Tensor:
+    """Fused remap, pull form: this rank reads its incoming rows straight from
+    the senders' IPC-shared buffers (``src``: attention layout for forward,
+    linear layout for inverse) over NVLink into ``out``."""
+    from . import _native
+    r = ctx.rank
+    a, b = layout.attn_rows[r], layout.linear_rows[r]
+    rows_in, rows_out = (b, a) if inverse else (a, b)
+    if out.shape[0] < rows_out:
+        raise ValueError(f"rank {r}: remap output needs {rows_out} rows")
+    _copy_prefix(out, src.buf[:rows_in], min(a, b), ctx)
+    tb = tables or pull_tables(layout, r, inverse, out.device)
+    src.epoch += 1
+    t = tb.table
+    stream = int(torch.cuda.current_stream().cuda_stream)
+    if copy_engine:
+        import ctypes
+        if src.host_ptrs is None:
+            src.host_ptrs = np.ascontiguousarray(src.peer_ptrs.cpu().numpy())
+        h = tb.host
+        ops._count_launch(2)
+        _native.call("zp_remap_pull_ce", out.data_ptr(), src.row_bytes, src.host_ptrs.ctypes.data,
+                     h[0].ctypes.data, h[1].ctypes.data, h[2].ctypes.data, src.flag_ptrs.data_ptr(),
+                     t[2].data_ptr(), t[3].data_ptr(), ctx.world, r, src.epoch, stream)
+        return out[:rows_out]
+    ops._count_launch(3)
+    _native.call("zp_remap_pull", out.data_ptr(), src.row_bytes, src.peer_ptrs.data_ptr(),
+                 t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), src.flag_ptrs.data_ptr(),
+                 t[3].data_ptr(), ctx.world, r, src.epoch, tb.max_count,
+                 int(torch.cuda.current_stream().cuda_stream))
+    return out[:rows_out]
 
 
 # ------------------------------------------------------------------ layer
@@ -362,11 +430,15 @@ class ZeppelinLayer:
     ``backward_layout(y)`` restores the attention layout."""
 
     def __init__(self, cluster, ctx: RankContext | None = None, n_heads: int = 32, n_kv_heads: int = 8,
-                 head_dim: int = 128):
+                 head_dim: int = 128, remap_method: str = "pull"):
         self.cluster = cluster
         self.ctx = ctx or RankContext.from_env()
         self.n_heads, self.n_kv_heads, self.head_dim = n_heads, n_kv_heads, head_dim
         self.plan = self.schedule = self.program = self.device_program = None
+        if remap_method not in ("pull", "push", "nccl"):
+            raise ValueError("remap_method must be 'pull', 'push' or 'nccl'")
+        self.remap_method = remap_method
+        self.peer: PeerBuffer | None = None
 
     def prepare(self, batch):
         self.plan = build_plan(batch, self.cluster)
@@ -382,10 +454,42 @@ class ZeppelinLayer:
     def attention(self, q, k, v):
         return attention_forward(self.plan, self.schedule, q, k, v, self.ctx, self.program, self.device_program)
 
+    def activation_buffer(self) -> torch.Tensor:
+        """[token_capacity, Hq*128] bf16 buffer shared over CUDA IPC (world > 1):
+        attention output lands in its prefix [0, A_r) and the remap turns it
+        into the linear layout [0, B_r) in place."""
+        if self.peer is None and self.ctx.world > 1 and self.remap_method != "nccl":
+            self.peer = PeerBuffer(self.ctx, self.cluster.token_capacity, self.n_heads * self.head_dim)
+        return self.peer.buf if self.peer is not None else None
+
     def forward(self, q, k, v):
-        o, lse = self.attention(q, k, v)
-        y = remap_forward(self.layout, o.view(o.shape[0], -1), self.ctx)
-        return o, lse, y
+        """Attention in the attention layout, then remap to the balanced linear
+        layout.  Returns (o, lse, y) with y [B_r, Hq*128]."""
+        buf = self.activation_buffer()
+        rows = q.shape[0]
+        if buf is None:
+            o, lse = self.attention(q, k, v)
+            return o, lse, remap_forward(self.layout, o.view(rows, -1), self.ctx)
+        o = buf[:rows].view(rows, self.n_heads, self.head_dim)
+        lse = torch.empty(self.n_heads, max(rows, 1), dtype=torch.float32, device=q.device)
+        attention_forward(self.plan, self.schedule, q, k, v, self.ctx, self.program, self.device_program,
+                          out=(o, lse))
+        if self.remap_method == "pull":
+            y = remap_pull(self.layout, self.peer, buf, self.ctx)
+        else:
+            y = remap_push(self.layout, buf[:rows], self.peer, self.ctx)
+        return o, lse, y[:self.layout.linear_rows[self.ctx.rank]]
 
     def backward_layout(self, y):
-        return remap_inverse(self.layout, y, self.ctx)
+        """Linear layout -> attention layout (exact inverse of the remap)."""
+        if self.peer is None:
+            return remap_inverse(self.layout, y, self.ctx)
+        r = self.ctx.rank
+        if y.data_ptr() != self.peer.buf.data_ptr():
+            self.peer.buf[:y.shape[0]].copy_(y)
+        if self.remap_method == "pull":
+            x = remap_pull(self.layout, self.peer, self.peer.buf, self.ctx, inverse=True)
+        else:
+            x = remap_push(self.layout, self.peer.buf[:self.layout.linear_rows[r]], self.peer, self.ctx,
+                           inverse=True)
+        return x[:self.layout.attn_rows[r]]

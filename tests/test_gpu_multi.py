@@ -61,14 +61,21 @@ def _worker(rank, world, port, lengths, results):
             bp = engine.remap_push(lay, yp, att, ctx, inverse=True)
             torch.cuda.synchronize()
             push_ok &= bool(torch.equal(bp[:, :2], ids[:, :2])) and bool((bp[:, 2] == it + 7).all())
+        # the layer API: attention into the IPC activation buffer + fused pull remap
+        layer = engine.ZeppelinLayer(cluster, ctx)
+        layer.prepare(batch)
+        lo, llse, ly = layer.forward(q, k, v)
+        o_copy = lo.clone()
+        lx = layer.backward_layout(ly)
         torch.cuda.synchronize()
+        layer_ok = bool(torch.equal(lx.view_as(o_copy), o_copy)) and bool(torch.equal(o_copy, o))
         f64 = lambda m: {s: t.double().numpy() for s, t in m.items()}  # noqa: E731
         ref, _ = OA.run_plan(plan, sched, f64(sq), f64(sk), f64(sv), 128 ** -0.5)
         err = float(np.abs(o.float().cpu().numpy() - ref[rank][0]).max()) if q.shape[0] else 0.0
         want = OR.source_map(list(lay.attn_rows), lay.matrix)[rank]
         perm_ok = bool(np.array_equal(y[:, :2].cpu().numpy(), want))
         back_ok = bool(torch.equal(back, ids))
-        results[rank] = (err, perm_ok, back_ok and push_ok, len(plan.ring_groups))
+        results[rank] = (err, perm_ok, back_ok and push_ok and layer_ok, len(plan.ring_groups))
     finally:
         dist.destroy_process_group()
 
