@@ -293,61 +293,51 @@ def run_gpu(args):
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(plan, sched, args.cpu_seconds)
-    print(json.dumps(line), flush=True)
+    emit(line)
     if world > 1:
         dist.destroy_process_group()
 
 
 def run_e2e(args, ctx, dev, rows, hq, hkv, d, host_plan, world, rank):
-    """Same metric through the public API with pinned host inputs: every step
-    copies q/k/v H2D and reads the attention output O back D2H."""
+    """Same metric through the public API (ZeppelinLayer.step_host) with pinned
+    HOST q/k/v: every step plans the batch, copies its inputs H2D and reads
+    the attention output (after the remap round trip) back D2H; copies of
+    neighbouring steps overlap compute on separate streams."""
     import torch
     import torch.distributed as dist
 
     from paper_2509_21841_b200 import engine
 
-    hq_d = hq * d
+    _, batch, cluster = workload(world)
+    layer = engine.ZeppelinLayer(cluster, ctx)
     hq_ = torch.randn(rows, hq, d, dtype=torch.bfloat16).pin_memory()
     hk_ = torch.randn(rows, hkv, d, dtype=torch.bfloat16).pin_memory()
     hv_ = torch.randn(rows, hkv, d, dtype=torch.bfloat16).pin_memory()
-    ho_ = torch.empty(rows, hq, d, dtype=torch.bfloat16).pin_memory()
+    ho_ = [torch.empty(rows, hq, d, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
 
-    def one():
-        plan_, sched_, prog_, devp_ = host_plan()
-        q = hq_.to(dev, non_blocking=True)
-        k = hk_.to(dev, non_blocking=True)
-        v = hv_.to(dev, non_blocking=True)
-        b_rows = prog_.remap.linear_rows[rank]
-        act = torch.empty(max(rows, b_rows, 1), hq_d, device=dev, dtype=torch.bfloat16)
-        lse = torch.empty(hq, max(rows, 1), device=dev)
-        engine.attention_forward(plan_, sched_, q, k, v, ctx, prog_, devp_, out=(act[:rows].view(rows, hq, d), lse))
-        y = engine.remap_forward(prog_.remap, act[:rows], ctx, out=act[:b_rows])
-        x = engine.remap_inverse(prog_.remap, y, ctx, out=act[:rows])
-        ho_.view(rows, hq_d).copy_(x, non_blocking=True)
+    def one(i):
+        layer.prepare(batch)
+        layer.step_host(hq_, hk_, hv_, ho_[i % 2])
 
-    for _ in range(max(1, args.warmup)):
-        one()
+    for i in range(max(1, args.warmup)):
+        one(i)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
-        one()
-    e1.record()
+    for i in range(args.steps):
+        one(i)
     torch.cuda.synchronize()
-    wall = (time.perf_counter() - t0) * 1e3 / args.steps
-    ms = max(e0.elapsed_time(e1) / args.steps, wall)
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    _, batch, _ = workload(world)
     return {"value": batch.total_tokens / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
             "h2d_bytes_per_step": int((hq_.numel() + hk_.numel() + hv_.numel()) * 2),
-            "d2h_bytes_per_step": int(ho_.numel() * 2),
-            "api": "paper_2509_21841_b200.engine.attention_forward + remap_forward + remap_inverse"}
+            "d2h_bytes_per_step": int(ho_[0].numel() * 2),
+            "timing": "wall clock over the steps incl. final sync, max over ranks",
+            "api": "paper_2509_21841_b200.ZeppelinLayer.prepare + step_host (pipelined H2D / D2H streams)"}
 
 
 def run_remap_stress(ctx, dev, world, rank, args, total=262144, iters=10):
@@ -502,7 +492,7 @@ def run_reference(args):
         remap_note = f"; + numpy remap fwd/inv of all ranks ({remap_s * 1e3:.0f} ms)"
     value = statistics.median(vals)
     ms = batch.total_tokens / value * 1e3
-    print(json.dumps({
+    emit({
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
@@ -510,10 +500,25 @@ def run_reference(args):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb["cores"], "kind": "port",
                          "sample": cb["sample"] + remap_note},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }), flush=True)
+    })
+
+
+_JSON_OUT = None
+
+
+def emit(line: dict) -> None:
+    """Print the single JSON result line on the ORIGINAL stdout (library
+    banners, e.g. NCCL's version line, are routed to stderr)."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 def main():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)  # everything else written to fd 1 (C libraries included) goes to stderr
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)

@@ -454,6 +454,89 @@ class ZeppelinLayer:
     def attention(self, q, k, v):
         return attention_forward(self.plan, self.schedule, q, k, v, self.ctx, self.program, self.device_program)
 
+    # ------------------------------------------------------------ host-fed steps
+    def step_host(self, q_h: torch.Tensor, k_h: torch.Tensor, v_h: torch.Tensor, o_h: torch.Tensor) -> None:
+        """One layer step fed from pinned HOST buffers, pipelined: the H2D of
+        this step's q/k/v runs on a copy stream while the previous step
+        computes, and the D2H of the attention output (after the remap round
+        trip) runs on a third stream while the next step computes.  Two device
+        slots (inputs + activation buffer) alternate.  Asynchronous: call
+        ``torch.cuda.synchronize()`` (or ``drain()``) before reading ``o_h``."""
+        ctx = self.ctx
+        dev = ctx.device
+        rows, hq, d = q_h.shape
+        if not hasattr(self, "_slots"):
+            self._slots = []
+            for _ in range(2):
+                uses_peer = ctx.world > 1 and self.remap_method != "nccl"
+                self._slots.append({"act": True if uses_peer else None, "free": torch.cuda.Event(),
+                                    "used": False})
+            self._h2d = torch.cuda.Stream(dev)
+            self._d2h = torch.cuda.Stream(dev)
+            self._turn = 0
+        slot = self._slots[self._turn]
+        self._turn ^= 1
+        key = (rows, hq, k_h.shape[1], d)
+        if slot.get("key") != key:
+            slot["q"] = torch.empty(rows, hq, d, dtype=torch.bfloat16, device=dev)
+            slot["k"] = torch.empty(rows, k_h.shape[1], d, dtype=torch.bfloat16, device=dev)
+            slot["v"] = torch.empty_like(slot["k"])
+            if slot["act"] is None:
+                slot["own_act"] = torch.empty(max(rows, max(self.layout.linear_rows), 1), hq * d,
+                                              dtype=torch.bfloat16, device=dev)
+            slot["key"] = key
+        cs = torch.cuda.current_stream(dev)
+        ready = torch.cuda.Event()
+        with torch.cuda.stream(self._h2d):
+            if slot["used"]:
+                self._h2d.wait_event(slot["free"])  # step i-2 no longer reads this slot's inputs
+            slot["q"].copy_(q_h, non_blocking=True)
+            slot["k"].copy_(k_h, non_blocking=True)
+            slot["v"].copy_(v_h, non_blocking=True)
+            ready.record(self._h2d)
+        cs.wait_event(ready)
+        if slot["used"]:
+            cs.wait_event(slot["d2h_done"])  # previous D2H of this slot's output finished
+        q, k, v = slot["q"], slot["k"], slot["v"]
+        if slot["act"] is not None:
+            peer = slot["peer_obj"] if "peer_obj" in slot else None
+            if peer is None:
+                peer = self._peer_for(slot)
+            act = peer.buf
+            o = act[:rows].view(rows, hq, d)
+            lse = torch.empty(hq, max(rows, 1), dtype=torch.float32, device=dev)
+            attention_forward(self.plan, self.schedule, q, k, v, ctx, self.program, self.device_program,
+                              out=(o, lse))
+            if self.remap_method == "pull":
+                remap_pull(self.layout, peer, act, ctx)
+                remap_pull(self.layout, peer, act, ctx, inverse=True)
+            else:
+                remap_push(self.layout, act[:rows], peer, ctx)
+                remap_push(self.layout, act[:self.layout.linear_rows[ctx.rank]], peer, ctx, inverse=True)
+            res = act[:rows]
+        else:
+            act = slot["own_act"]
+            o = act[:rows].view(rows, hq, d)
+            lse = torch.empty(hq, max(rows, 1), dtype=torch.float32, device=dev)
+            attention_forward(self.plan, self.schedule, q, k, v, ctx, self.program, self.device_program,
+                              out=(o, lse))
+            y = remap_forward(self.layout, act[:rows], ctx, out=act[:self.layout.linear_rows[ctx.rank]])
+            res = remap_inverse(self.layout, y, ctx, out=act[:rows])
+        slot["free"].record(cs)
+        done = torch.cuda.Event()
+        with torch.cuda.stream(self._d2h):
+            self._d2h.wait_event(slot["free"])
+            o_h.view(rows, -1).copy_(res, non_blocking=True)
+            done.record(self._d2h)
+        slot["d2h_done"] = done
+        slot["used"] = True
+
+    def _peer_for(self, slot) -> "PeerBuffer":
+        peer = PeerBuffer(self.ctx, self.cluster.token_capacity, self.n_heads * self.head_dim)
+        slot["peer_obj"] = peer
+        slot["act"] = peer.buf
+        return peer
+
     def activation_buffer(self) -> torch.Tensor:
         """[token_capacity, Hq*128] bf16 buffer shared over CUDA IPC (world > 1):
         attention output lands in its prefix [0, A_r) and the remap turns it
