@@ -514,6 +514,78 @@ def emit(line: dict) -> None:
     out.flush()
 
 
+def run_block(args):
+    """Config 5: full Llama-3-8B block (norm, QKV, remap, RoPE, attention,
+    remap, O, norm, SwiGLU MLP) on the 256K-token github<=128K batch (seed 1)
+    over N GPUs; tokens/s of the whole block, same JSON contract."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_21841_b200 import block as B, engine, ops
+    from paper_2509_21841_b200 import workloads as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    ctx = engine.RankContext(rank, world, dev)
+    batch = W.c4_batch()
+    cluster = W.cluster_for(batch, world)
+    w = B.BlockWeights.random(dev, seed=0)
+    blk = B.ZeppelinBlock(cluster, w, ctx, max_pos=262144)
+    blk.prepare(batch)
+    a, b = blk.rows
+    x = torch.randn(b, B.HIDDEN, device=dev, dtype=torch.bfloat16)
+
+    def step():
+        blk.prepare(batch)
+        return blk.forward(x)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ops.reset_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    gemm, attn = blk.flops_per_step()
+    fl = torch.tensor([float(gemm), float(attn)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(fl)
+    peak, peak_sus, _, kind = _peaks()
+    total_tf = float(fl.sum()) / (ms / 1e3) / 1e12
+    line = {
+        "metric": "full transformer block tokens/s (config 5)", "value": batch.total_tokens / (ms / 1e3),
+        "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init Llama-3-8B block weights, N(0,1) hidden states)",
+        "config": {"workload": "C5: Llama-3-8B block, 256K-token github<=128K batch (seed 1)",
+                   "total_tokens": batch.total_tokens, "rings": len(blk.plan.ring_groups),
+                   "remap_rows_moved": int(blk.layout.moved_rows()),
+                   "gemms": "cuBLAS bf16 (torch.matmul/addmm)"},
+        "tflops_aggregate": total_tf, "tflops_per_gpu": total_tf / world,
+        "frac_of_peak_per_gpu": total_tf / world / peak, "gemm_flop": float(fl[0]), "attn_flop": float(fl[1]),
+        "gpu_launches": ops.launch_count(), "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        emit(line)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     global _JSON_OUT
     sys.stdout.flush()
@@ -528,11 +600,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-remap-stress", action="store_true")
+    ap.add_argument("--workload", choices=["layer", "c5"], default="layer",
+                    help="layer: attn+remap (BASELINE metric); c5: full transformer block")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "zeppelin":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "c5":
+        run_block(args)
     else:
         run_gpu(args)
 

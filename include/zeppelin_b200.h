@@ -152,6 +152,24 @@ ZP_API int zp_remap_push_ce(const void* src, int64_t row_bytes, const int64_t* d
                      const int32_t* count_dev, const int32_t* expect_dev, int world,
                      int my_rank, int32_t epoch, void* stream);
 
+/* ---- full transformer block (config 5): elementwise kernels around the
+ * cuBLAS GEMMs of the linear modules, which run on the balanced (linear)
+ * layout as in the reference's linear phase (simulator.py:291-299). */
+
+/* y = x / sqrt(mean(x^2) + eps) * w, rows x hidden bf16 (hidden % 8 == 0, <= 8192). */
+ZP_API int zp_rmsnorm(const void* x, const void* w, void* y, int rows, int hidden, float eps,
+               void* stream);
+
+/* Split qkv [rows, (hq+2*hkv)*128] bf16 (attention layout) into q [rows,hq,128],
+ * k, v [rows,hkv,128]; q and k rotated (rotate-half RoPE) at each row's GLOBAL
+ * in-sequence position pos[row], cos/sin from fp32 tables [max_pos, 64]. */
+ZP_API int zp_rope_split(const void* qkv, const int32_t* pos, const float* cos_table,
+                  const float* sin_table, void* q, void* k, void* v, int rows, int hq,
+                  int hkv, int head_dim, void* stream);
+
+/* a = silu(g) * u for gu = [rows, 2*inter] = [g | u] bf16 -> out [rows, inter]. */
+ZP_API int zp_swiglu(const void* gu, void* out, int rows, int inter, void* stream);
+
 /* CUDA IPC helpers for zp_remap_push (host pointers to 64-byte handles).
  * get_handle exports the allocation containing dev_ptr and returns dev_ptr's
  * byte offset inside it; a peer maps it with open_handle and adds the offset. */

@@ -34,6 +34,9 @@ SIGNATURES: dict[str, tuple] = {
                                   ctypes.c_int32, _vp]),
     "zp_remap_push_ce": (_c_int, [_vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                   ctypes.c_int32, _vp]),
+    "zp_rmsnorm": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_float, _vp]),
+    "zp_rope_split": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
+    "zp_swiglu": (_c_int, [_vp, _vp, _c_int, _c_int, _vp]),
     "zp_ipc_get_handle": (_c_int, [_vp, _vp, ctypes.POINTER(_c_i64)]),
     "zp_ipc_open_handle": (_c_int, [_vp, ctypes.POINTER(_vp)]),
     "zp_ipc_close_handle": (_c_int, [_vp]),

@@ -151,3 +151,37 @@ def copy_rows(dst: torch.Tensor, src: torch.Tensor, ranges: torch.Tensor, n_rang
     _native.call("zp_copy_rows", dst.data_ptr(), dst.stride(0) * dst.element_size(), src.data_ptr(),
                  src.stride(0) * src.element_size(), row_bytes, ranges.data_ptr(), n_ranges,
                  max_rows, _stream_ptr(stream))
+
+
+# ---------------------------------------------------------------- block kernels
+
+def rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float = 1e-5, out: torch.Tensor | None = None) -> torch.Tensor:
+    _require_cuda(x, w)
+    y = out if out is not None else torch.empty_like(x)
+    _count_launch()
+    _native.call("zp_rmsnorm", x.data_ptr(), w.data_ptr(), y.data_ptr(), x.shape[0], x.shape[1], eps,
+                 _stream_ptr())
+    return y
+
+
+def rope_split(qkv: torch.Tensor, pos: torch.Tensor, cos_t: torch.Tensor, sin_t: torch.Tensor,
+               hq: int, hkv: int):
+    """qkv [rows, (hq+2hkv)*128] -> q [rows,hq,128], k/v [rows,hkv,128] (q, k rotated)."""
+    _require_cuda(qkv, pos, cos_t, sin_t)
+    rows = qkv.shape[0]
+    q = torch.empty(rows, hq, 128, dtype=qkv.dtype, device=qkv.device)
+    k = torch.empty(rows, hkv, 128, dtype=qkv.dtype, device=qkv.device)
+    v = torch.empty_like(k)
+    _count_launch()
+    _native.call("zp_rope_split", qkv.data_ptr(), pos.data_ptr(), cos_t.data_ptr(), sin_t.data_ptr(),
+                 q.data_ptr(), k.data_ptr(), v.data_ptr(), rows, hq, hkv, 128, _stream_ptr())
+    return q, k, v
+
+
+def swiglu(gu: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    _require_cuda(gu)
+    rows, two_inter = gu.shape
+    y = out if out is not None else torch.empty(rows, two_inter // 2, dtype=gu.dtype, device=gu.device)
+    _count_launch()
+    _native.call("zp_swiglu", gu.data_ptr(), y.data_ptr(), rows, two_inter // 2, _stream_ptr())
+    return y

@@ -91,3 +91,50 @@ def test_multi_gpu_attention_and_remap(lengths):
     assert sorted(res) == list(range(world))
     for rank, (err, perm_ok, back_ok, nrings) in res.items():
         assert err <= 2e-2 and perm_ok and back_ok, res
+
+
+def _block_worker(rank, world, port, lengths, results):
+    import torch.distributed as dist
+    from paper_2509_21841_b200 import block as B, engine
+    from paper_2509_21841_b200.batch import SequenceBatch
+    from paper_2509_21841_b200.cluster import single_box
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        batch = SequenceBatch(tuple(enumerate(lengths)))
+        cluster = single_box(world, batch.total_tokens)
+        w = B.BlockWeights.random("cuda", seed=3)
+        blk = B.ZeppelinBlock(cluster, w, engine.RankContext(rank, world), max_pos=8192)
+        plan = blk.prepare(batch)
+        g = torch.Generator(device="cuda").manual_seed(5)
+        x_seq = {s: torch.randn(n, 4096, device="cuda", generator=g).to(torch.bfloat16)
+                 for s, n in enumerate(lengths)}
+        toks = B.linear_tokens(plan, blk.layout, rank)
+        x = torch.stack([x_seq[int(s)][int(p)] for s, p in toks])
+        out = blk.forward(x)
+        out2 = blk.forward(x)  # second pass exercises the remap epochs
+        torch.cuda.synchronize()
+        ref = B.reference_block(x_seq, w)
+        want = torch.stack([ref[int(s)][int(p)] for s, p in toks])
+        err = (out.float() - want).abs()
+        scale = want.abs().max().item()
+        results[rank] = (err.max().item() / scale, err.mean().item() / scale, bool(torch.equal(out, out2)),
+                         len(plan.ring_groups), int(blk.layout.moved_rows()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_multi_gpu_full_block_matches_fp32_reference():
+    world = min(torch.cuda.device_count(), 4)
+    lengths = [2500, 300, 700, 90, 1000]
+    with mp.Manager() as mgr:
+        res = mgr.dict()
+        mp.spawn(_block_worker, args=(world, _port(), lengths, res), nprocs=world, join=True)
+        res = dict(res)
+    assert sorted(res) == list(range(world))
+    assert any(v[3] > 0 for v in res.values()), "config must exercise rings"
+    for rank, (emax, emean, same, nr, moved) in res.items():
+        assert emax <= 3e-2 and emean <= 3e-3 and same, res
