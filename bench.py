@@ -586,6 +586,88 @@ def run_block(args):
         dist.destroy_process_group()
 
 
+def run_compare(args):
+    """the paper's comparison executed, not modelled.  The
+    same batch runs under zeppelin, te_cp, llama_cp and hybrid_dp plans
+    (reference baselines.py) on the same GPUs; per strategy the full Llama-3-8B
+    block (config 5 code path) and its attention+remap part are timed."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_21841_b200 import block as B, engine, ops
+    from paper_2509_21841_b200 import workloads as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    ctx = engine.RankContext(rank, world, dev)
+    batch = W.c4_batch()  # 256K-token long-tailed github<=128K batch (configs 4/5)
+    cluster = W.cluster_for(batch, world)
+    w = B.BlockWeights.random(dev, seed=0)
+    results = {}
+    for strategy in ("zeppelin", "te_cp", "llama_cp", "hybrid_dp"):
+        try:
+            blk = B.ZeppelinBlock(cluster, w, ctx, max_pos=262144, strategy=strategy)
+            blk.prepare(batch)
+        except Exception as exc:  # e.g. InfeasibleBatch under the even split
+            results[strategy] = {"error": f"{type(exc).__name__}: {exc}"}
+            continue
+        a, b = blk.rows
+        x = torch.randn(b, B.HIDDEN, device=dev, dtype=torch.bfloat16)
+        q = torch.randn(a, 32, 128, device=dev, dtype=torch.bfloat16)
+        k = torch.randn(a, 8, 128, device=dev, dtype=torch.bfloat16)
+        v = torch.randn(a, 8, 128, device=dev, dtype=torch.bfloat16)
+        o = torch.empty_like(q)
+        lse = torch.empty(32, max(a, 1), device=dev)
+        kvx = "allgather" if strategy == "llama_cp" else "ring"
+
+        def attn_step():
+            engine.attention_forward(blk.plan, blk.schedule, q, k, v, ctx, blk.program, blk.device_program,
+                                     out=(o, lse), kv_exchange=kvx)
+            if blk.peer_o is not None:
+                blk.peer_o.buf[:a].copy_(o.view(a, -1))
+                engine.remap_pull(blk.layout, blk.peer_o, blk.peer_o.buf, ctx)
+                engine.remap_pull(blk.layout, blk.peer_o, blk.peer_o.buf, ctx, inverse=True)
+
+        res = {"rows_per_rank_max": max(blk.plan.tokens_per_rank), "rings": len(blk.plan.ring_groups)}
+        for name, fn in (("attention_layer", attn_step), ("block", lambda: blk.forward(x))):
+            for _ in range(args.warmup):
+                fn()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.steps):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev, dtype=torch.float64)
+            if world > 1:
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            res[name] = {"ms": ms, "tokens_per_s": batch.total_tokens / (ms / 1e3)}
+        results[strategy] = res
+        del blk, q, k, v, o, x
+        torch.cuda.empty_cache()
+    z = results.get("zeppelin", {})
+    for sname, r in results.items():
+        if "error" not in r and "error" not in z:
+            r["zeppelin_speedup_block"] = r["block"]["ms"] / z["block"]["ms"]
+            r["zeppelin_speedup_attention_layer"] = r["attention_layer"]["ms"] / z["attention_layer"]["ms"]
+    if rank == 0:
+        emit({"metric": "strategy comparison (block and attention+remap ms, max over ranks)",
+              "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+              "config": {"workload": "C4/C5 batch: 256K-token github<=128K (seed 1)", "total_tokens": batch.total_tokens,
+                         "sequences": len(batch)}, "results": results})
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     global _JSON_OUT
     sys.stdout.flush()
@@ -600,7 +682,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-remap-stress", action="store_true")
-    ap.add_argument("--workload", choices=["layer", "c5"], default="layer",
+    ap.add_argument("--workload", choices=["layer", "c5", "compare"], default="layer",
                     help="layer: attn+remap (BASELINE metric); c5: full transformer block")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "zeppelin":
@@ -609,6 +691,8 @@ def main():
         run_reference(args)
     elif args.workload == "c5":
         run_block(args)
+    elif args.workload == "compare":
+        run_compare(args)
     else:
         run_gpu(args)
 

@@ -91,10 +91,11 @@ def run_plan(plan, schedule, seq_q, seq_k, seq_v, scale, dtype=np.float64):
         n = sum(f.tokens for f in plan.fragments[rank])
         hq, d = next(iter(seq_q.values())).shape[1:]
         results.append((np.zeros((n, hq, d), dtype=dtype), np.full((hq, n), -np.inf, dtype=dtype)))
+    in_ring = {s.sequence_id for rs in schedule.rings() for s in rs.ring.sequences}
     for rank in range(plan.num_ranks):
         o, lse = results[rank]
         for f in plan.fragments[rank]:
-            if zone.get(f.sequence_id) == "local" or f.micro_batch > 0:
+            if (zone.get(f.sequence_id) == "local" or f.micro_batch > 0) and f.sequence_id not in in_ring:
                 row0, n = rows_of[rank][(f.sequence_id, f.start)]
                 pos = np.arange(f.start, f.end)
                 oo, ll, _ = causal_attention(seq_q[f.sequence_id][f.start:f.end], seq_k[f.sequence_id][f.start:f.end],

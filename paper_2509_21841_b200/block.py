@@ -97,25 +97,32 @@ class ZeppelinBlock:
     """One Llama-3-8B block for this rank (one process per GPU)."""
 
     def __init__(self, cluster, weights: BlockWeights, ctx: engine.RankContext | None = None,
-                 max_pos: int = 262144):
+                 max_pos: int = 262144, strategy: str = "zeppelin"):
         self.cluster = cluster
+        self.strategy = strategy
         self.w = weights
         self.ctx = ctx or engine.RankContext.from_env()
         self.cos, self.sin = rope_tables(max_pos, self.ctx.device)
         self.hq = weights.w_o.shape[1] // HEAD_DIM
         self.hkv = (weights.w_qkv.shape[0] // HEAD_DIM - self.hq) // 2
         self.peer_qkv = self.peer_o = None
-        if self.ctx.world > 1:
+        if self.ctx.world > 1 and strategy == "zeppelin":
             cap = cluster.token_capacity
             self.peer_qkv = engine.PeerBuffer(self.ctx, cap, weights.w_qkv.shape[0])
             self.peer_o = engine.PeerBuffer(self.ctx, cap, self.hq * HEAD_DIM)
 
     def prepare(self, batch):
         r = self.ctx.rank
-        self.plan = build_plan(batch, self.cluster)
+        if self.strategy == "zeppelin":
+            self.plan = build_plan(batch, self.cluster)
+            lay = solve_remap(self.plan.tokens_per_rank, cost_matrix(self.cluster))
+        else:  # comparison strategies: no remap, linear modules on the attention layout
+            from .baselines import plan_for
+            from .remap import identity_layout
+            self.plan = plan_for(self.strategy, batch, self.cluster)
+            lay = identity_layout(self.plan.tokens_per_rank)
         self.schedule = build_schedule(self.plan)
-        res = solve_remap(self.plan.tokens_per_rank, cost_matrix(self.cluster))
-        self.program = build_rank_program(self.plan, self.schedule, r, self.hq, res)
+        self.program = build_rank_program(self.plan, self.schedule, r, self.hq, lay)
         self.device_program = engine.DeviceProgram(self.program, self.ctx.device)
         self.layout = self.program.remap
         pos = attention_positions(self.plan, r)
@@ -150,7 +157,7 @@ class ZeppelinBlock:
         o = o_buf[:a].view(a, self.hq, HEAD_DIM)
         lse = torch.empty(self.hq, max(a, 1), dtype=torch.float32, device=x.device)
         engine.attention_forward(self.plan, self.schedule, q, k, v, ctx, self.program, self.device_program,
-                                 out=(o, lse))
+                                 out=(o, lse), kv_exchange="allgather" if self.strategy == "llama_cp" else "ring")
         if self.peer_o is not None:
             engine.remap_pull(self.layout, self.peer_o, o_buf, ctx)
         x2 = torch.addmm(x, o_buf[:b], w.w_o.t())

@@ -162,10 +162,38 @@ def _run_ring(ctx: RankContext, rp, dev_pack, dev_rounds, q, k, v, o, lse, scale
         cs.wait_stream(xs)  # buffers / sends complete before the next ring reuses them
 
 
+def _run_ring_allgather(ctx: RankContext, rp, dev_pack, dev_rounds, q, k, v, o, lse, scale):
+    """LLaMA-CP style execution of a ring (reference baselines.py:114-117,
+    simulator.py:227-262): every member all-gathers the ring's KV sets first
+    (one NCCL all-gather, not overlapped), then runs all rounds back to back."""
+    hkv, d = k.shape[1], k.shape[2]
+    hq = q.shape[1]
+    g = rp.group_size
+    rows = max(rp.held_rows)
+    gathered = ctx.workspace("ring_allgather", (g, rows, 2, hkv, d), torch.bfloat16)
+    mine = ctx.workspace("ring_allgather_mine", (rows, 2, hkv, d), torch.bfloat16)
+    st_o = ctx.workspace("ring_state_o", (max(rp.state_rows, 1), hq, d), torch.float32)
+    st_ml = ctx.workspace("ring_state_ml", (2, hq, max(rp.state_rows, 1)), torch.float32)
+    n_pack = rp.pack_ranges.shape[0]
+    max_pack = int(rp.pack_ranges[:, 2].max()) if n_pack else 0
+    ops.copy_rows(mine[:, 0], k, dev_pack, n_pack, max_pack)
+    ops.copy_rows(mine[:, 1], v, dev_pack, n_pack, max_pack)
+    if g != ctx.world or tuple(rp.members) != tuple(range(ctx.world)):
+        raise ValueError("all-gather KV exchange needs a ring over every rank (LLaMA-CP layout)")
+    dist.all_gather_into_tensor(gathered, mine, group=ctx.group)
+    for r in range(g):
+        work = dev_rounds[r]
+        buf = gathered[rp.rounds[r].src_position]
+        n_kv = rp.rounds[r].kv_rows
+        if work.n:
+            ops.attn_fwd(q, buf[:n_kv, 0], buf[:n_kv, 1], work.items, work.n, work.segs, o, lse,
+                         st_o, st_ml, softmax_scale=scale)
+
+
 def attention_forward(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
                       ctx: RankContext | None = None, program: RankProgram | None = None,
                       device_program: DeviceProgram | None = None, softmax_scale: float | None = None,
-                      out: tuple[torch.Tensor, torch.Tensor] | None = None):
+                      out: tuple[torch.Tensor, torch.Tensor] | None = None, kv_exchange: str = "ring"):
     """This rank's attention (LocalTasks + every RingRound it takes part in).
 
     q [A_r, Hq, 128], k/v [A_r, Hkv, 128] bf16 in the rank's attention layout
@@ -185,8 +213,9 @@ def attention_forward(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torch
         o, lse = out
     if devp.local.n:
         ops.attn_fwd(q, k, v, devp.local.items, devp.local.n, devp.local.segs, o, lse, softmax_scale=scale)
+    run = _run_ring_allgather if kv_exchange == "allgather" else _run_ring
     for rp, (pack, rounds) in zip(prog.rings, devp.rings):
-        _run_ring(ctx, rp, pack, rounds, q, k, v, o, lse, scale)
+        run(ctx, rp, pack, rounds, q, k, v, o, lse, scale)
     return o, lse
 
 
@@ -344,6 +373,8 @@ def remap_push(layout: RemapLayout, x: torch.Tensor, peer: PeerBuffer, ctx: Rank
         raise ValueError(f"rank {r}: remap input has {x.shape[0]} rows, layout says {rows_in}")
     out = peer.buf[:rows_out]
     _copy_prefix(out, x, min(a, b), ctx)
+    if layout.moved_rows() == 0:
+        return out
     tb = tables or push_tables(layout, r, inverse, x.device)
     peer.epoch += 1
     t = tb.table
@@ -397,6 +428,8 @@ def remap_pull(layout: RemapLayout, src: PeerBuffer, out: torch.Tensor, ctx: Ran
     if out.shape[0] < rows_out:
         raise ValueError(f"rank {r}: remap output needs {rows_out} rows")
     _copy_prefix(out, src.buf[:rows_in], min(a, b), ctx)
+    if layout.moved_rows() == 0:
+        return out[:rows_out]
     tb = tables or pull_tables(layout, r, inverse, out.device)
     src.epoch += 1
     t = tb.table

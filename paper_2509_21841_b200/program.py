@@ -108,13 +108,17 @@ def build_rank_program(plan, schedule: AttentionSchedule, rank: int, n_heads: in
     frag_rows: dict[tuple[int, int], int] = {}
     at = 0
     local_frags: list[QueryFragment] = []
+    # A sequence that rides a ring is computed by its ring rounds only.  (The
+    # even-split baselines label a short ring member LOCAL when it lands on one
+    # rank; the reference cost model then charges it twice, execution must not.)
+    in_ring = {s.sequence_id for rs in schedule.rings() for s in rs.ring.sequences}
     for f in plan.fragments[rank]:
         frag_rows[(f.sequence_id, f.start)] = at
-        if plan.zone_of.get(f.sequence_id) == LOCAL or f.micro_batch > 0:
+        if (plan.zone_of.get(f.sequence_id) == LOCAL or f.micro_batch > 0) and f.sequence_id not in in_ring:
             local_frags.append(QueryFragment(row0=at, pos0=0, length=f.tokens, segs=[(at, 0, f.tokens)]))
         at += f.tokens
     local = build_worklist(local_frags, n_hp)
-    want = sum(t.compute_pairs for t in schedule.local_tasks if t.rank == rank)
+    want = sum(t.compute_pairs for t in schedule.local_tasks if t.rank == rank and t.sequence_id not in in_ring)
     if local.pairs_per_head != want:
         raise AssertionError(f"rank {rank}: local work list covers {local.pairs_per_head} pairs, schedule says {want}")
 

@@ -308,3 +308,11 @@ def remap_layout(counts: list[int], result: RemapResult | None = None,
         result = solve_remap(counts, cost)
     return RemapLayout(attn_rows=tuple(counts), linear_rows=tuple(target_distribution(counts)),
                        matrix=np.asarray(result.matrix, dtype=np.int64))
+
+
+def identity_layout(counts: list[int]) -> RemapLayout:
+    """No remap: the linear modules run on the attention layout (what the
+    comparison strategies do; only Zeppelin rebalances)."""
+    counts = [int(c) for c in counts]
+    return RemapLayout(attn_rows=tuple(counts), linear_rows=tuple(counts),
+                       matrix=np.zeros((len(counts), len(counts)), dtype=np.int64))

@@ -138,3 +138,53 @@ def test_multi_gpu_full_block_matches_fp32_reference():
     assert any(v[3] > 0 for v in res.values()), "config must exercise rings"
     for rank, (emax, emean, same, nr, moved) in res.items():
         assert emax <= 3e-2 and emean <= 3e-3 and same, res
+
+
+def _strategy_worker(rank, world, port, lengths, results):
+    import torch.distributed as dist
+    from oracle import attention as OA
+    from paper_2509_21841_b200 import engine, schedule as S
+    from paper_2509_21841_b200.baselines import plan_for
+    from paper_2509_21841_b200.batch import SequenceBatch
+    from paper_2509_21841_b200.cluster import single_box
+    from paper_2509_21841_b200.emulate import gather_rank
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        batch = SequenceBatch(tuple(enumerate(lengths)))
+        cluster = single_box(world, batch.total_tokens, slack=1.5)
+        g = torch.Generator().manual_seed(2)
+        seqs = sorted(batch.lengths.items())
+        sq = {s: torch.randn(n, 8, 128, generator=g).to(torch.bfloat16) for s, n in seqs}
+        sk = {s: torch.randn(n, 2, 128, generator=g).to(torch.bfloat16) for s, n in seqs}
+        sv = {s: torch.randn(n, 2, 128, generator=g).to(torch.bfloat16) for s, n in seqs}
+        f64 = lambda m: {s: t.double().numpy() for s, t in m.items()}  # noqa: E731
+        out = {}
+        for strategy in ("te_cp", "llama_cp", "hybrid_dp"):
+            plan = plan_for(strategy, batch, cluster)
+            sched = S.build_schedule(plan)
+            q, k, v = (gather_rank(x, plan, rank, "cuda") for x in (sq, sk, sv))
+            o, lse = engine.attention_forward(plan, sched, q, k, v, engine.RankContext(rank, world),
+                                              kv_exchange="allgather" if strategy == "llama_cp" else "ring")
+            torch.cuda.synchronize()
+            ref, _ = OA.run_plan(plan, sched, f64(sq), f64(sk), f64(sv), 128 ** -0.5)
+            out[strategy] = float(np.abs(o.float().cpu().numpy() - ref[rank][0]).max()) if q.shape[0] else 0.0
+        results[rank] = out
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_comparison_strategies_execute_exactly():
+    world = min(torch.cuda.device_count(), 4)
+    lengths = [3000, 40, 700, 1200, 90]
+    with mp.Manager() as mgr:
+        res = mgr.dict()
+        mp.spawn(_strategy_worker, args=(world, _port(), lengths, res), nprocs=world, join=True)
+        res = dict(res)
+    assert sorted(res) == list(range(world))
+    for rank, errs in res.items():
+        for strategy, err in errs.items():
+            assert err <= 2e-2, (rank, strategy, err)

@@ -26,7 +26,9 @@ if os.path.isdir(REF):
     from varlenplan import routing as rrt
     from varlenplan import topology as rt
     from varlenplan import workload as rw
+    from varlenplan import baselines as rb
 
+from paper_2509_21841_b200 import baselines as BL
 from paper_2509_21841_b200 import batch as B
 from paper_2509_21841_b200 import cluster as C
 from paper_2509_21841_b200 import plan as P
@@ -169,3 +171,32 @@ def test_intermediate_levels_match():
             assert (ia.s0, ia.restarts) == (ib.s0, ib.restarts)
             assert [[(e.sequence_id, e.start, e.end, e.kind) for e in d] for d in ia.devices] == \
                    [[(e.sequence_id, e.start, e.end, e.kind) for e in d] for d in ib.devices]
+
+
+@pytest.mark.parametrize("strategy", ["te_cp", "llama_cp", "hybrid_dp"])
+def test_baseline_planners_bit_exact(strategy):
+    rng = random.Random(17)
+    fn_ref = {"te_cp": rb.plan_te_cp, "llama_cp": rb.plan_llama_cp, "hybrid_dp": rb.plan_hybrid_dp}[strategy]
+    fn_me = {"te_cp": BL.plan_te_cp, "llama_cp": BL.plan_llama_cp, "hybrid_dp": BL.plan_hybrid_dp}[strategy]
+    cases = []
+    for _ in range(300):
+        n, p, cap = rng.choice([1, 2]), rng.choice([1, 2, 4, 8]), rng.randint(4, 60)
+        cases.append(([rng.randint(1, n * p * cap // 2 + 1) for _ in range(rng.randint(1, 7))], (n, p, cap, 1.0, 2.0)))
+    inv = 4096 / 900e9
+    for g in (2, 4, 8):
+        for name in ("arxiv", "github", "prolong64k"):
+            for seed in range(3):
+                seqs = rw.sample_batch(rw.preset(name), 262144, seed).sequences
+                cases.append(([n for _, n in seqs], (1, g, -(-1050 * 262144 // (1000 * g)), inv, inv)))
+    for lengths, args in cases:
+        rb_, mb_ = rw.SequenceBatch(tuple(enumerate(lengths))), B.SequenceBatch(tuple(enumerate(lengths)))
+        try:
+            a = fn_ref(rb_, rt.ClusterSpec(*args))
+        except Exception as exc:
+            with pytest.raises(Exception) as info:
+                fn_me(mb_, C.ClusterSpec(*args))
+            assert (type(info.value).__name__, str(info.value)) == (type(exc).__name__, str(exc))
+            continue
+        b = fn_me(mb_, C.ClusterSpec(*args))
+        assert rp.plan_to_json(a) == P.plan_to_json(b)
+        assert sched_tuple(ra.build_schedule(a)) == sched_tuple(S.build_schedule(b))
