@@ -141,15 +141,18 @@ class ZeppelinBlock:
         w, ctx = self.w, self.ctx
         if x.shape[0] != b:
             raise ValueError(f"rank {ctx.rank}: block input has {x.shape[0]} rows, linear layout has {b}")
-        h = ops.rmsnorm(x, w.attn_norm, EPS)
+        with ctx.span("compute", "linear", {"tokens": b, "op": "attn_norm+qkv"}):
+            h = ops.rmsnorm(x, w.attn_norm, EPS)
+            if self.peer_qkv is not None:
+                qkv_buf = self.peer_qkv.buf
+                torch.matmul(h, w.w_qkv.t(), out=qkv_buf[:b])
+            else:
+                qkv = torch.matmul(h, w.w_qkv.t())
         if self.peer_qkv is not None:
-            qkv_buf = self.peer_qkv.buf
-            torch.matmul(h, w.w_qkv.t(), out=qkv_buf[:b])
             engine.remap_pull(self.layout, self.peer_qkv, qkv_buf, ctx, inverse=True)
             qkv = qkv_buf[:a]
-        else:
-            qkv = torch.matmul(h, w.w_qkv.t())
-        q, k, v = ops.rope_split(qkv, self.pos, self.cos, self.sin, self.hq, self.hkv)
+        with ctx.span("compute", "rope", {"tokens": a}):
+            q, k, v = ops.rope_split(qkv, self.pos, self.cos, self.sin, self.hq, self.hkv)
         if self.peer_o is not None:
             o_buf = self.peer_o.buf
         else:
@@ -160,11 +163,12 @@ class ZeppelinBlock:
                                  out=(o, lse), kv_exchange="allgather" if self.strategy == "llama_cp" else "ring")
         if self.peer_o is not None:
             engine.remap_pull(self.layout, self.peer_o, o_buf, ctx)
-        x2 = torch.addmm(x, o_buf[:b], w.w_o.t())
-        h2 = ops.rmsnorm(x2, w.mlp_norm, EPS)
-        gu = torch.matmul(h2, w.w_gu.t())
-        act = ops.swiglu(gu)
-        return torch.addmm(x2, act, w.w_down.t())
+        with ctx.span("compute", "linear", {"tokens": b, "op": "o+mlp"}):
+            x2 = torch.addmm(x, o_buf[:b], w.w_o.t())
+            h2 = ops.rmsnorm(x2, w.mlp_norm, EPS)
+            gu = torch.matmul(h2, w.w_gu.t())
+            act = ops.swiglu(gu)
+            return torch.addmm(x2, act, w.w_down.t())
 
     def flops_per_step(self) -> tuple[int, int]:
         """(GEMM FLOPs, attention FLOPs) of this rank's step."""

@@ -45,6 +45,13 @@ class RankContext:
         self.group = group
         self.comm_stream = torch.cuda.Stream(self.device) if world > 1 else None
         self._ws: dict[str, torch.Tensor] = {}
+        self.tracer = None  # trace.Tracer: measured timeline in the reference trace schema
+
+    def span(self, stream_name: str, kind: str, payload: dict | None = None, stream=None):
+        import contextlib
+        if self.tracer is None:
+            return contextlib.nullcontext()
+        return self.tracer.span(stream_name, kind, payload, stream)
 
     @classmethod
     def from_env(cls) -> "RankContext":
@@ -140,20 +147,24 @@ def _run_ring(ctx: RankContext, rp, dev_pack, dev_rounds, q, k, v, o, lse, scale
             xs.wait_event(ready)
             if done is not None:
                 xs.wait_event(done)  # round r-1 finished reading nxt
-            with torch.cuda.stream(xs):
+            with torch.cuda.stream(xs), ctx.span("intra-comm", "kv.send",
+                                                  {"ring": rp.ring_index, "round": r, "tokens": rp.send_rows(r),
+                                                   "dst": rp.next_rank}, xs):
                 p2p = ring_p2p_ops(rp, r, cur, nxt, ctx.group)
                 if p2p:
                     for req in dist.batch_isend_irecv(p2p):
                         req.wait()
-                nxt_ready = torch.cuda.Event()
-                nxt_ready.record(xs)
+            nxt_ready = torch.cuda.Event()
+            nxt_ready.record(xs)
         if r > 0:
             cs.wait_event(ready)
         work = dev_rounds[r]
         n_kv = rp.rounds[r].kv_rows
-        if work.n:
-            ops.attn_fwd(q, cur[:n_kv, 0], cur[:n_kv, 1], work.items, work.n, work.segs, o, lse,
-                         st_o, st_ml, softmax_scale=scale)
+        with ctx.span("compute", "intra_node.attn",
+                      {"ring": rp.ring_index, "round": r, "pairs": rp.rounds[r].work.pairs_per_head}):
+            if work.n:
+                ops.attn_fwd(q, cur[:n_kv, 0], cur[:n_kv, 1], work.items, work.n, work.segs, o, lse,
+                             st_o, st_ml, softmax_scale=scale)
         done = torch.cuda.Event()
         done.record(cs)
         if nxt_ready is not None:
@@ -180,7 +191,8 @@ def _run_ring_allgather(ctx: RankContext, rp, dev_pack, dev_rounds, q, k, v, o, 
     ops.copy_rows(mine[:, 1], v, dev_pack, n_pack, max_pack)
     if g != ctx.world or tuple(rp.members) != tuple(range(ctx.world)):
         raise ValueError("all-gather KV exchange needs a ring over every rank (LLaMA-CP layout)")
-    dist.all_gather_into_tensor(gathered, mine, group=ctx.group)
+    with ctx.span("intra-comm", "kv.allgather", {"tokens": int(rp.held_rows[rp.position])}):
+        dist.all_gather_into_tensor(gathered, mine, group=ctx.group)
     for r in range(g):
         work = dev_rounds[r]
         buf = gathered[rp.rounds[r].src_position]
@@ -212,7 +224,8 @@ def attention_forward(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torch
     else:
         o, lse = out
     if devp.local.n:
-        ops.attn_fwd(q, k, v, devp.local.items, devp.local.n, devp.local.segs, o, lse, softmax_scale=scale)
+        with ctx.span("compute", "local.attn", {"pairs": prog.local.pairs_per_head, "items": devp.local.n}):
+            ops.attn_fwd(q, k, v, devp.local.items, devp.local.n, devp.local.segs, o, lse, softmax_scale=scale)
     run = _run_ring_allgather if kv_exchange == "allgather" else _run_ring
     for rp, (pack, rounds) in zip(prog.rings, devp.rings):
         run(ctx, rp, pack, rounds, q, k, v, o, lse, scale)
@@ -445,7 +458,8 @@ def remap_pull(layout: RemapLayout, src: PeerBuffer, out: torch.Tensor, ctx: Ran
                      t[2].data_ptr(), t[3].data_ptr(), ctx.world, r, src.epoch, stream)
         return out[:rows_out]
     ops._count_launch(3)
-    _native.call("zp_remap_pull", out.data_ptr(), src.row_bytes, src.peer_ptrs.data_ptr(),
+    with ctx.span("intra-comm", "remap.inverse" if inverse else "remap.forward", {"tokens": int(tb.host[2].sum())}):
+        _native.call("zp_remap_pull", out.data_ptr(), src.row_bytes, src.peer_ptrs.data_ptr(),
                  t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), src.flag_ptrs.data_ptr(),
                  t[3].data_ptr(), ctx.world, r, src.epoch, tb.max_count,
                  int(torch.cuda.current_stream().cuda_stream))
