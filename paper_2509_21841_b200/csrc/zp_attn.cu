@@ -8,57 +8,113 @@
 // the KV set held by the ring position (i-r) mod g, resuming the running
 // softmax state of the previous round (exact online-softmax continuation).
 //
-// CTA = one work item = 128 query rows x 2 query heads of one GQA group.
-//   warp 0      TMA producer (Q, then K/V tiles through 2-stage rings)
-//   warp 1      TMEM allocator + tcgen05.mma issuer (single thread)
+// Work item = 128 query rows x 2 query heads of one GQA group.  Two variants of
+// one kernel template:
+//
+//   single (kPair=false): one CTA per item, M=128 tcgen05.mma (cta_group::1).
+//   pair   (kPair=true):  a cluster of 2 CTAs on one TPC runs items 2p and 2p+1
+//       (heads 4g..4g+3 of one KV head) as M=256 tcgen05.mma.cta_group::2: each
+//       CTA holds its own Q rows, HALF of every K tile (64 keys) and HALF of
+//       every V tile (64 dims); the leader CTA issues all MMAs for the pair and
+//       each CTA's TMEM receives its own 128 rows.  Per SM this halves the
+//       shared-memory operand traffic of B (K, V) and the K/V bytes fetched,
+//       which is what bounds the single-CTA M=128 pipeline.
+//
+// Roles inside a CTA (384 threads):
+//   warp 0      TMA producer (Q, then K/V tiles through smem rings); in the
+//               pair the leader's producer also claims work items
+//   warp 1      TMEM allocator + tcgen05.mma issuer (single thread; leader only)
 //   warps 2-3   idle (keep warpgroup 0 whole for setmaxnreg)
-//   warps 4-7   softmax / rescale / epilogue for head 2p   (thread == row)
-//   warps 8-11  softmax / rescale / epilogue for head 2p+1 (thread == row)
+//   warps 4-7   softmax / rescale / epilogue for head tile 0 (thread == row)
+//   warps 8-11  softmax / rescale / epilogue for head tile 1 (thread == row)
 // A warp may only touch TMEM lanes 32*(warp%4)..+31.  Warpgroup 0 gives its
 // registers to the two softmax warpgroups (setmaxnreg), which hold a whole
 // 128-column S row per thread.
 // TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512);
 // P_t (bf16x2 packed, 64 columns) aliases S_t columns [64,128) and feeds the
-// PV product as the TMEM A operand.  Shared memory: Q0,Q1 (2x32 KB), K and V
-// 2-stage rings (4x32 KB), all SWIZZLE_128B as written by TMA.
+// PV product as the TMEM A operand.  Shared memory: Q0,Q1 (2x32 KB) and the
+// K and V rings, all SWIZZLE_128B as written by TMA.
+#include <cstdlib>
+
 #include "zp_ptx.cuh"
 #include "../../include/zeppelin_b200.h"
 
 namespace zp {
 
 constexpr int kHeadDim = 128;
-constexpr int kBM = 128;  // query rows per tile
+constexpr int kBM = 128;  // query rows per CTA tile
 constexpr int kBN = 128;  // key rows per tile
 constexpr int kThreads = 384;
 constexpr uint32_t kTileBytes = kBM * kHeadDim * 2;   // 32 KB
-constexpr uint32_t kBoxBytes = 128 * 64 * 2;          // 16 KB (one 64-column TMA box)
-constexpr uint32_t kSmemQ = 0;
-constexpr uint32_t kSmemK = 2 * kTileBytes;
-constexpr uint32_t kSmemV = 4 * kTileBytes;
-constexpr uint32_t kSmemBar = 6 * kTileBytes;
-constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;  // + barriers/sched ring + alignment slack
+constexpr uint32_t kBoxBytes = 128 * 64 * 2;          // 16 KB (one 64-column x 128-row TMA box)
 constexpr int kSchedSlots = 4;
+#ifndef ZP_MMA_UNROLL
+#define ZP_MMA_UNROLL 8
+#endif
+#ifndef ZP_WG0_REGS
+#define ZP_WG0_REGS 88  // producer / MMA warpgroup; the softmax warpgroups get 208
+#endif
+constexpr int kMmaUnroll = ZP_MMA_UNROLL;
 
-// barrier slots
+// Diagnostic build only (-DZP_TRACE): SM clock stamps of CTA 0's softmax
+// stages and MMA issue points, read back with zp_debug_trace().
+#ifdef ZP_TRACE
+__device__ unsigned long long g_zp_trace[4096];
+#define ZP_STAMP(slot)                                                              \
+  do {                                                                              \
+    if (blockIdx.x == 0 && (slot) >= 0 && (slot) < 4096) {                          \
+      unsigned long long c_;                                                        \
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_)::"memory");                  \
+      g_zp_trace[slot] = c_;                                                        \
+    }                                                                               \
+  } while (0)
+#else
+#define ZP_STAMP(slot) \
+  do {                 \
+  } while (0)
+#endif
+static_assert(ZP_WG0_REGS * 128 + 208 * 256 <= 168 * 384, "setmaxnreg exceeds the launch register pool");
+
+template <bool kPair>
+struct Cfg {
+  static constexpr int kKStages = kPair ? 4 : 2;
+  static constexpr int kVStages = kPair ? 4 : 2;
+  // bytes of one K / V ring stage in THIS CTA (the pair splits each tile)
+  static constexpr uint32_t kKBytes = kPair ? kTileBytes / 2 : kTileBytes;
+  static constexpr uint32_t kVBytes = kPair ? kTileBytes / 2 : kTileBytes;
+  static constexpr uint32_t kKRows = kPair ? kBN / 2 : kBN;  // key rows of K per CTA
+  static constexpr uint32_t kKBox = kKRows * 128;            // one 64-column K box
+  static constexpr uint32_t kSmemQ = 0;
+  static constexpr uint32_t kSmemK = 2 * kTileBytes;
+  static constexpr uint32_t kSmemV = kSmemK + kKStages * kKBytes;
+  static constexpr uint32_t kSmemBar = kSmemV + kVStages * kVBytes;
+  static constexpr uint32_t kSmemBytes = kSmemBar + 512 + 1024;  // barriers/sched ring + alignment slack
+  static constexpr uint32_t kPFullCount = kPair ? 8 : 4;          // one arrival per softmax warp (x CTAs)
+  static constexpr uint32_t kSchedConsumers = kPair ? 18 : 9;
+};
+
+// barrier slots (ring stages <= 4)
 enum : int {
   B_QFULL = 0,
-  B_KFULL = 1,   // +stage
-  B_KEMPTY = 3,  // +stage
-  B_VFULL = 5,   // +stage
-  B_VEMPTY = 7,  // +stage
-  B_SFULL = 9,   // +tile
-  B_PFULL = 11,  // +tile
-  B_ODONE = 13,  // +tile
-  B_QEMPTY = 15,
-  B_SCHED_FULL = 16,   // +slot (4): item index published by the producer
-  B_SCHED_EMPTY = 20,  // +slot (4): consumed by the MMA warp and 8 softmax warps
-  B_COUNT = 24
+  B_KFULL = 1,          // +stage
+  B_KEMPTY = 5,         // +stage
+  B_VFULL = 9,          // +stage
+  B_VEMPTY = 13,        // +stage
+  B_SFULL = 17,         // +tile
+  B_PFULL = 19,         // +2*tile+half: P columns of keys [0,64) / [64,128) stored
+  B_ODONE = 23,         // +tile
+  B_QEMPTY = 25,
+  B_SCHED_FULL = 26,    // +slot (4): item index published by the producer
+  B_SCHED_EMPTY = 30,   // +slot (4): consumed by the MMA issuer and the softmax warps
+  B_COUNT = 34
 };
+static_assert(Cfg<true>::kKStages <= 4 && Cfg<true>::kVStages <= 4, "ring depth <= 4");
+static_assert(Cfg<true>::kSmemBytes <= 232448 && Cfg<false>::kSmemBytes <= 232448, "smem budget");
 
 struct AttnArgs {
   const zp_attn_item* items;
-  int n_items;
-  int* next_item;  // global work counter (zeroed before the launch)
+  int n_units;     // items (single) or item pairs (pair)
+  int* next_unit;  // global work counter (zeroed before the launch)
   const zp_kv_seg* segs;
   __nv_bfloat16* o;
   float* lse;
@@ -96,11 +152,7 @@ struct TileCursor {
   __device__ __forceinline__ int valid() const { return min(kBN, g.len - ti * kBN); }
 };
 
-#ifndef ZP_EMU_OF8
-#define ZP_EMU_OF8 0
-#endif
-constexpr float kRescaleLog2 = 8.0f;     // lazy-rescale threshold (log2 units)
-constexpr int kEmuOf8 = ZP_EMU_OF8;      // column pairs per 8 whose exp2 runs on the FMA pipe
+constexpr float kRescaleLog2 = 8.0f;  // lazy-rescale threshold (log2 units)
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
@@ -108,15 +160,20 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   return r;
 }
 
+#ifndef ZP_EMU_OF8
+#define ZP_EMU_OF8 0
+#endif
+constexpr int kEmuOf8 = ZP_EMU_OF8;  // column pairs per 8 whose exp2 runs on the FMA pipe
+
 // 2^x for a pair on the FMA pipe: round-to-nearest split x = j + f (magic
 // constant 1.5*2^23), degree-3 minimax polynomial for 2^f on [-1/2, 1/2]
 // (max rel. error 7.5e-5, far below bf16's 3.9e-3), exponent add for 2^j.
-// x is clamped at -125 so the exponent add never underflows (2^-125 ~ 0).
+// x is clamped at -125 so the exponent add never underflows (2^-125 ~ 0);
+// used on unmasked tiles only (masked keys need an exact 0).
 __device__ __forceinline__ float2 exp2_poly(float2 x) {
   x.x = fmaxf(x.x, -125.f);
   x.y = fmaxf(x.y, -125.f);
-  const float2 magic = make_float2(12582912.f, 12582912.f);
-  const float2 y = __fadd2_rn(x, magic);
+  const float2 y = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
   const float2 j = __fadd2_rn(y, make_float2(-12582912.f, -12582912.f));
   const float2 f = __ffma2_rn(j, make_float2(-1.f, -1.f), x);
   float2 p = __ffma2_rn(make_float2(0.055171608583694395f, 0.055171608583694395f), f,
@@ -127,15 +184,15 @@ __device__ __forceinline__ float2 exp2_poly(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(y.y) << 23)));
 }
 
-// P = 2^(s*scale_log2 - m) for one 128-column row, packed to bf16x2 and
-// stored to the row's P columns in TMEM; row sum accumulated in two float2.
-// kEmu: a fixed share of column pairs takes the FMA-pipe exp2 (never on
-// masked tiles: -inf must give exactly 0).
-template <bool kEmu>
-__device__ __forceinline__ void exp_tile(const float (&s)[128], float2 sl2x2, float2 negm, uint32_t tP,
+// P = 2^(s*scale_log2 - m) for one half (64 keys) of a 128-column row,
+// packed to bf16x2 and stored to the half's 32 P columns in TMEM; row sum
+// accumulated in two float2.  kEmu: a fixed share of the column pairs takes
+// the FMA-pipe exp2 (relieves the MUFU pipe, 16 ex2/clk/SM).
+template <int kHalf, bool kEmu>
+__device__ __forceinline__ void exp_half(const float (&s)[128], float2 sl2x2, float2 negm, uint32_t tP,
                                          float2& acc0, float2& acc1) {
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 2 * kHalf; c < 2 * kHalf + 2; ++c) {
     uint32_t pk[16];
 #pragma unroll
     for (int v = 0; v < 16; ++v) {
@@ -154,43 +211,42 @@ __device__ __forceinline__ void exp_tile(const float (&s)[128], float2 sl2x2, fl
   }
 }
 
+template <bool kPair>
+__device__ __forceinline__ void commit(uint32_t bar) {
+  if constexpr (kPair) tc_commit_pair(bar, 0x3);
+  else tc_commit(bar);
+}
+
 // Descriptor start addresses are in 16-byte units in the low 14 bits, so a
 // byte offset inside shared memory is added to a base descriptor as off>>4.
+// K tile (this CTA's rows) is K-major: 16 dims per MMA, the two 64-dim halves
+// are one K box apart.
+template <bool kPair>
 __device__ __forceinline__ void issue_qk(uint32_t d_tmem, uint64_t q_desc, uint64_t k_desc,
                                          uint32_t idesc) {
-#pragma unroll
+#pragma unroll kMmaUnroll
   for (int kk = 0; kk < kHeadDim / 16; ++kk) {
-    const uint64_t off = ((kk >> 2) * kBoxBytes + (kk & 3) * 32) >> 4;
-    mma_ss(d_tmem, q_desc + off, k_desc + off, idesc, kk > 0 ? 1u : 0u);
+    const uint64_t qoff = ((kk >> 2) * kBoxBytes + (kk & 3) * 32) >> 4;
+    const uint64_t koff = ((kk >> 2) * Cfg<kPair>::kKBox + (kk & 3) * 32) >> 4;
+    if constexpr (kPair) mma_ss_pair(d_tmem, q_desc + qoff, k_desc + koff, idesc, kk > 0 ? 1u : 0u);
+    else mma_ss(d_tmem, q_desc + qoff, k_desc + koff, idesc, kk > 0 ? 1u : 0u);
   }
 }
 
-// V tile is [128 keys x 128 dims], dims contiguous: MN-major B operand.  16
-// keys per MMA = 2 groups of 8 rows (SBO 1 KB); the two 64-dim swizzle atoms
-// are one TMA box apart (LBO 16 KB).  P (A operand) is 8 TMEM columns per
-// 16 keys.
+// V tile is [128 keys x dims], dims contiguous: MN-major B operand.  16 keys
+// per MMA = 2 groups of 8 rows (SBO 1 KB); in the single kernel the two 64-dim
+// swizzle atoms are one TMA box apart (LBO 16 KB), in the pair each CTA holds
+// one 64-dim atom.  P (A operand) is 8 TMEM columns per 16 keys.
+template <bool kPair>
 __device__ __forceinline__ void issue_pv(uint32_t d_tmem, uint32_t p_tmem, uint64_t v_desc,
-                                         uint32_t idesc, bool accumulate) {
+                                         uint32_t idesc, bool accumulate, int half) {
 #pragma unroll
-  for (int kk = 0; kk < kBN / 16; ++kk)
-    mma_ts(d_tmem, p_tmem + kk * 8, v_desc + uint64_t(kk * (2048 >> 4)), idesc,
-           (accumulate || kk > 0) ? 1u : 0u);
-}
-
-// Persistent, dynamically scheduled CTAs: the producer thread claims the next
-// item of the longest-first list with one atomicAdd (greedy LPT across SMs)
-// and publishes it to the MMA and softmax warps through a 4-slot smem ring.
-struct SchedRing {
-  uint32_t bar_full, bar_empty;  // barrier addresses of slot 0
-  volatile int* idx;             // kSchedSlots published item indices
-  __device__ __forceinline__ int consume(uint32_t k, bool arrive) const {
-    const uint32_t slot = k % kSchedSlots;
-    mbar_wait(bar_full + 8 * slot, (k / kSchedSlots) & 1);
-    const int v = idx[slot];
-    if (arrive) mbar_arrive(bar_empty + 8 * slot);
-    return v;
+  for (int kk = 4 * half; kk < 4 * half + 4; ++kk) {
+    const uint32_t acc = (accumulate || kk > 0) ? 1u : 0u;
+    if constexpr (kPair) mma_ts_pair(d_tmem, p_tmem + kk * 8, v_desc + uint64_t(kk * (2048 >> 4)), idesc, acc);
+    else mma_ts(d_tmem, p_tmem + kk * 8, v_desc + uint64_t(kk * (2048 >> 4)), idesc, acc);
   }
-};
+}
 
 __device__ __forceinline__ int count_tiles(const zp_kv_seg* segs, const zp_attn_item& it) {
   int n = 0;
@@ -199,50 +255,82 @@ __device__ __forceinline__ int count_tiles(const zp_kv_seg* segs, const zp_attn_
   return n;
 }
 
+// Persistent, dynamically scheduled CTAs (CTA pairs): the producer thread (the
+// leader's, in a pair) claims the next unit of the longest-first list with one
+// atomicAdd (greedy LPT across SMs) and publishes it to every consumer through
+// a 4-slot smem ring (both CTAs' rings in a pair).
+template <bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const AttnArgs args) {
+  using C = Cfg<kPair>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t sbase = (raw + 1023u) & ~1023u;
   uint8_t* sgen = smem_raw + (sbase - raw);
-  const uint32_t bar0 = sbase + kSmemBar;
+  const uint32_t bar0 = sbase + C::kSmemBar;
   auto bar = [&](int i) -> uint32_t { return bar0 + 8u * uint32_t(i); };
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sgen + kSmemBar + 8 * B_COUNT);
-  const SchedRing ring{bar(B_SCHED_FULL), bar(B_SCHED_EMPTY),
-                       reinterpret_cast<volatile int*>(sgen + kSmemBar + 8 * B_COUNT + 16)};
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sgen + C::kSmemBar + 8 * B_COUNT);
+  volatile int* ring_idx = reinterpret_cast<volatile int*>(sgen + C::kSmemBar + 8 * B_COUNT + 16);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int n_items = args.n_items;
+  const int n_units = args.n_units;
+  const uint32_t cta = kPair ? cluster_ctarank() : 0u;
+  // barrier of the MMA-issuing (leader) CTA, as a shared::cluster address
+  auto lead = [&](int i) -> uint32_t { return kPair ? mapa_shared(bar(i), 0) : bar(i); };
 
   if (threadIdx.x == 0) {
     mbar_init(bar(B_QFULL), 1);
     mbar_init(bar(B_QEMPTY), 1);
     for (int k = 0; k < kSchedSlots; ++k) {
       mbar_init(bar(B_SCHED_FULL + k), 1);
-      mbar_init(bar(B_SCHED_EMPTY + k), 9);  // MMA thread + one lane per softmax warp
+      mbar_init(bar(B_SCHED_EMPTY + k), C::kSchedConsumers);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < C::kKStages; ++s) {
       mbar_init(bar(B_KFULL + s), 1);
       mbar_init(bar(B_KEMPTY + s), 1);
+    }
+    for (int s = 0; s < C::kVStages; ++s) {
       mbar_init(bar(B_VFULL + s), 1);
       mbar_init(bar(B_VEMPTY + s), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(bar(B_SFULL + s), 1);
-      mbar_init(bar(B_PFULL + s), 128);
+      mbar_init(bar(B_PFULL + 2 * s), C::kPFullCount);
+      mbar_init(bar(B_PFULL + 2 * s + 1), C::kPFullCount);
       mbar_init(bar(B_ODONE + s), 1);
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(smem_u32(tmem_slot), 512);
+  if (warp == 1) {
+    if constexpr (kPair) tmem_alloc_pair(smem_u32(tmem_slot), 512);
+    else tmem_alloc(smem_u32(tmem_slot), 512);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync_all();  // peer barriers initialised before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // Next work unit for a consumer: wait for the slot, then release it to the
+  // publishing producer (leader's ring in a pair).
+  auto sched_wait = [&](uint32_t k) -> int {
+    const uint32_t slot = k % kSchedSlots;
+    // the peer CTA's ring is written remotely by the leader: cluster-scope acquire
+    if (kPair && cta != 0) mbar_wait_cluster(bar(B_SCHED_FULL + slot), (k / kSchedSlots) & 1);
+    else mbar_wait(bar(B_SCHED_FULL + slot), (k / kSchedSlots) & 1);
+    return ring_idx[slot];
+  };
+  auto sched_release = [&](uint32_t k) {
+    const uint32_t slot = k % kSchedSlots;
+    if constexpr (kPair) mbar_arrive_cluster(lead(B_SCHED_EMPTY + slot));
+    else mbar_arrive(bar(B_SCHED_EMPTY + slot));
+  };
+
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(ZP_WG0_REGS));
     if (warp == 0 && lane == 0) {
       // ---------------- producer: per item Q (2 heads), then K_j / V_j rings
       tma_prefetch_desc(&tm_q);
@@ -252,115 +340,145 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_kv = policy_evict_last();
       uint32_t jg = 0, qn = 0;
       for (uint32_t k = 0;; ++k) {
-        const uint32_t slot = k % kSchedSlots;
-        if (k >= kSchedSlots) mbar_wait(bar(B_SCHED_EMPTY + slot), ((k / kSchedSlots) - 1) & 1);
-        const int idx = atomicAdd(args.next_item, 1);
-        ring.idx[slot] = idx;
-        mbar_arrive(bar(B_SCHED_FULL + slot));
-        if (idx >= n_items) break;
-        const zp_attn_item it = args.items[idx];
+        int idx;
+        if (cta == 0) {
+          const uint32_t slot = k % kSchedSlots;
+          if (k >= kSchedSlots) {
+            if constexpr (kPair) mbar_wait_cluster(bar(B_SCHED_EMPTY + slot), ((k / kSchedSlots) - 1) & 1);
+            else mbar_wait(bar(B_SCHED_EMPTY + slot), ((k / kSchedSlots) - 1) & 1);
+          }
+          idx = atomicAdd(args.next_unit, 1);
+          ring_idx[slot] = idx;
+          if constexpr (kPair) {
+            const uint32_t peer_idx = mapa_shared(smem_u32(const_cast<int*>(ring_idx + slot)), 1);
+            st_cluster_u32(peer_idx, uint32_t(idx));
+            mbar_arrive_cluster(mapa_shared(bar(B_SCHED_FULL + slot), 1));
+          }
+          mbar_arrive(bar(B_SCHED_FULL + slot));
+        } else {
+          idx = sched_wait(k);
+          sched_release(k);
+        }
+        if (idx >= n_units) break;
+        const zp_attn_item it = args.items[kPair ? 2 * idx + int(cta) : idx];
         if (count_tiles(args.segs, it) == 0) continue;
         const int kvh = (2 * it.head_pair) / args.group;
         if (qn > 0) mbar_wait(bar(B_QEMPTY), (qn - 1) & 1);
-        mbar_expect_tx(bar(B_QFULL), 2 * kTileBytes);
+        if (cta == 0) mbar_expect_tx(bar(B_QFULL), (kPair ? 4 : 2) * kTileBytes);
         for (int t = 0; t < 2; ++t)
-          for (int b = 0; b < 2; ++b)
-            tma_load_2d(sbase + kSmemQ + t * kTileBytes + b * kBoxBytes, &tm_q, bar(B_QFULL),
-                        (2 * it.head_pair + t) * kHeadDim + b * 64, it.q_row0, pol_q);
+          for (int b = 0; b < 2; ++b) {
+            const uint32_t dst = sbase + C::kSmemQ + t * kTileBytes + b * kBoxBytes;
+            const int x = (2 * it.head_pair + t) * kHeadDim + b * 64;
+            if constexpr (kPair) tma_load_2d_pair(dst, &tm_q, lead(B_QFULL), x, it.q_row0, pol_q);
+            else tma_load_2d(dst, &tm_q, bar(B_QFULL), x, it.q_row0, pol_q);
+          }
         ++qn;
         TileCursor cur(args.segs, it.seg_begin, it.seg_count, it.q_pos0 + it.q_len - 1);
         for (; cur.next(); ++jg) {
-          const int st = jg & 1;
-          const uint32_t u = jg >> 1;
+          const int kst = int(jg % C::kKStages), vst = int(jg % C::kVStages);
+          const uint32_t ku = jg / C::kKStages, vu = jg / C::kVStages;
           const int row = cur.row();
-          if (jg >= 2) mbar_wait(bar(B_KEMPTY + st), (u - 1) & 1);
-          mbar_expect_tx(bar(B_KFULL + st), kTileBytes);
-          for (int b = 0; b < 2; ++b)
-            tma_load_2d(sbase + kSmemK + st * kTileBytes + b * kBoxBytes, &tm_k, bar(B_KFULL + st),
-                        kvh * kHeadDim + b * 64, row, pol_kv);
-          if (jg >= 2) mbar_wait(bar(B_VEMPTY + st), (u - 1) & 1);
-          mbar_expect_tx(bar(B_VFULL + st), kTileBytes);
-          for (int b = 0; b < 2; ++b)
-            tma_load_2d(sbase + kSmemV + st * kTileBytes + b * kBoxBytes, &tm_v, bar(B_VFULL + st),
-                        kvh * kHeadDim + b * 64, row, pol_kv);
+          if (jg >= uint32_t(C::kKStages)) mbar_wait(bar(B_KEMPTY + kst), (ku - 1) & 1);
+          if (cta == 0) mbar_expect_tx(bar(B_KFULL + kst), (kPair ? 2 : 1) * C::kKBytes);
+          for (int b = 0; b < 2; ++b) {
+            const uint32_t dst = sbase + C::kSmemK + kst * C::kKBytes + b * C::kKBox;
+            if constexpr (kPair)
+              tma_load_2d_pair(dst, &tm_k, lead(B_KFULL + kst), kvh * kHeadDim + b * 64,
+                               row + int(cta) * (kBN / 2), pol_kv);
+            else
+              tma_load_2d(dst, &tm_k, bar(B_KFULL + kst), kvh * kHeadDim + b * 64, row, pol_kv);
+          }
+          if (jg >= uint32_t(C::kVStages)) mbar_wait(bar(B_VEMPTY + vst), (vu - 1) & 1);
+          if (cta == 0) mbar_expect_tx(bar(B_VFULL + vst), (kPair ? 2 : 1) * C::kVBytes);
+          if constexpr (kPair) {
+            tma_load_2d_pair(sbase + C::kSmemV + vst * C::kVBytes, &tm_v, lead(B_VFULL + vst),
+                             kvh * kHeadDim + int(cta) * 64, row, pol_kv);
+          } else {
+            for (int b = 0; b < 2; ++b)
+              tma_load_2d(sbase + C::kSmemV + vst * C::kVBytes + b * kBoxBytes, &tm_v, bar(B_VFULL + vst),
+                          kvh * kHeadDim + b * 64, row, pol_kv);
+          }
         }
       }
-    } else if (warp == 1 && lane == 0) {
+    } else if (warp == 1 && lane == 0 && cta == 0) {
       // ---------------- MMA issuer.  Global tile stream: at tile g it issues
       // PV_t(g-1) then S_t(g) for t = 0, 1 (the S/P TMEM aliasing relies on
       // tcgen05 MMAs executing in issue order).
-      constexpr uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
-      constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
+      constexpr uint32_t idesc_qk = idesc_bf16_f32(kPair ? 256 : 128, 128, 0, 0);
+      constexpr uint32_t idesc_pv = idesc_bf16_f32(kPair ? 256 : 128, 128, 0, 1);
       const uint32_t tS[2] = {tmem + 0, tmem + 128};
       const uint32_t tO[2] = {tmem + 256, tmem + 384};
-      const uint64_t q_desc0 = umma_desc_sw128(sbase + kSmemQ, 16, 1024);
-      const uint64_t k_desc0 = umma_desc_sw128(sbase + kSmemK, 16, 1024);
-      const uint64_t v_desc0 = umma_desc_sw128(sbase + kSmemV, kBoxBytes, 1024);
-      const uint64_t vk_step = kTileBytes >> 4;  // one 32 KB tile, in descriptor units
+      const uint64_t q_desc0 = umma_desc_sw128(sbase + C::kSmemQ, 16, 1024);
+      const uint64_t k_desc0 = umma_desc_sw128(sbase + C::kSmemK, 16, 1024);
+      const uint64_t v_desc0 = umma_desc_sw128(sbase + C::kSmemV, kBoxBytes, 1024);
+      constexpr uint64_t q_step = kTileBytes >> 4, k_step = C::kKBytes >> 4, v_step = C::kVBytes >> 4;
       uint32_t jg = 0, qn = 0;
       bool prev_acc = false;  // accumulate flag of the pending PV (tile jg-1)
+      // PV_t of the previous tile, one 64-key half as soon as its P lands
+      auto pv_prev = [&](int t, int pvs) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait(bar(B_PFULL + 2 * t + h), (jg - 1) & 1);
+          tc_fence_after();
+          if (h == 0 && jg < 256) ZP_STAMP(2560 + int(jg) * 4 + 2 * t);
+          issue_pv<kPair>(tO[t], tS[t] + 64, v_desc0 + v_step * pvs, idesc_pv, prev_acc, h);
+        }
+        commit<kPair>(bar(B_ODONE + t));
+      };
       for (uint32_t k = 0;; ++k) {
-        const int idx = ring.consume(k, true);
-        if (idx >= n_items) break;
-        const zp_attn_item it = args.items[idx];
+        const int idx = sched_wait(k);
+        sched_release(k);
+        if (idx >= n_units) break;
+        const zp_attn_item it = args.items[kPair ? 2 * idx : idx];
         const int n = count_tiles(args.segs, it);
         if (n == 0) continue;
         const bool resume = (it.flags & ZP_ITEM_LOAD_STATE) != 0;
         for (int j = 0; j < n; ++j, ++jg) {
-          const int st = jg & 1, pst = (jg - 1) & 1;
+          const int kst = int(jg % C::kKStages);
+          const uint32_t kpar = (jg / C::kKStages) & 1;
+          const int pvs = int((jg - 1) % C::kVStages);
           if (jg > 0) {
-            mbar_wait(bar(B_VFULL + pst), ((jg - 1) >> 1) & 1);
+            mbar_wait(bar(B_VFULL + pvs), ((jg - 1) / C::kVStages) & 1);
             tc_fence_after();
           }
           if (j == 0) {
             // item boundary: finish the previous item's PVs first so its
             // epilogue is not held up by this item's Q load
             if (jg > 0) {
-              for (int t = 0; t < 2; ++t) {
-                mbar_wait(bar(B_PFULL + t), (jg - 1) & 1);
-                tc_fence_after();
-                issue_pv(tO[t], tS[t] + 64, v_desc0 + vk_step * pst, idesc_pv, prev_acc);
-                tc_commit(bar(B_ODONE + t));
-              }
+              for (int t = 0; t < 2; ++t) pv_prev(t, pvs);
             }
             mbar_wait(bar(B_QFULL), qn & 1);
-            mbar_wait(bar(B_KFULL + st), (jg >> 1) & 1);
+            mbar_wait(bar(B_KFULL + kst), kpar);
             tc_fence_after();
             for (int t = 0; t < 2; ++t) {
-              issue_qk(tS[t], q_desc0 + vk_step * t, k_desc0 + vk_step * st, idesc_qk);
-              tc_commit(bar(B_SFULL + t));
+              issue_qk<kPair>(tS[t], q_desc0 + q_step * t, k_desc0 + k_step * kst, idesc_qk);
+              commit<kPair>(bar(B_SFULL + t));
+              if (jg < 256) ZP_STAMP(2560 + int(jg) * 4 + 2 * t + 1);
             }
           } else {
             for (int t = 0; t < 2; ++t) {
-              mbar_wait(bar(B_PFULL + t), (jg - 1) & 1);
-              tc_fence_after();
-              issue_pv(tO[t], tS[t] + 64, v_desc0 + vk_step * pst, idesc_pv, prev_acc);
-              tc_commit(bar(B_ODONE + t));
+              pv_prev(t, pvs);
               if (t == 0) {
-                mbar_wait(bar(B_KFULL + st), (jg >> 1) & 1);
+                mbar_wait(bar(B_KFULL + kst), kpar);
                 tc_fence_after();
               }
-              issue_qk(tS[t], q_desc0 + vk_step * t, k_desc0 + vk_step * st, idesc_qk);
-              tc_commit(bar(B_SFULL + t));
+              issue_qk<kPair>(tS[t], q_desc0 + q_step * t, k_desc0 + k_step * kst, idesc_qk);
+              commit<kPair>(bar(B_SFULL + t));
+              if (jg < 256) ZP_STAMP(2560 + int(jg) * 4 + 2 * t + 1);
             }
           }
-          if (jg > 0) tc_commit(bar(B_VEMPTY + pst));
-          tc_commit(bar(B_KEMPTY + st));
-          if (j == n - 1) tc_commit(bar(B_QEMPTY));  // Q free once this item's S MMAs land
+          if (jg > 0) commit<kPair>(bar(B_VEMPTY + pvs));
+          commit<kPair>(bar(B_KEMPTY + kst));
+          if (j == n - 1) commit<kPair>(bar(B_QEMPTY));  // Q free once this item's S MMAs land
           prev_acc = resume || j > 0;
         }
         ++qn;
       }
       if (jg > 0) {
-        const int pst = (jg - 1) & 1;
-        mbar_wait(bar(B_VFULL + pst), ((jg - 1) >> 1) & 1);
+        const int pvs = int((jg - 1) % C::kVStages);
+        mbar_wait(bar(B_VFULL + pvs), ((jg - 1) / C::kVStages) & 1);
         tc_fence_after();
-        for (int t = 0; t < 2; ++t) {
-          mbar_wait(bar(B_PFULL + t), (jg - 1) & 1);
-          tc_fence_after();
-          issue_pv(tO[t], tS[t] + 64, v_desc0 + vk_step * pst, idesc_pv, prev_acc);
-          tc_commit(bar(B_ODONE + t));
-        }
+        for (int t = 0; t < 2; ++t) pv_prev(t, pvs);
       }
     }
   } else {
@@ -373,14 +491,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tS = tmem + lane_bits + uint32_t(t * 128);
     const uint32_t tP = tS + 64;
     const uint32_t tO = tmem + lane_bits + 256u + uint32_t(t * 128);
+    const uint32_t pfull = lead(B_PFULL + 2 * t);  // + 8 bytes: second half
     const float sl2 = args.scale_log2;
     uint32_t jg = 0;
     for (uint32_t k = 0;; ++k) {
-      const int idx = ring.consume(k, false);
+      const int idx = sched_wait(k);
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar(B_SCHED_EMPTY + (k % kSchedSlots)));
-      if (idx >= n_items) break;
-      const zp_attn_item it = args.items[idx];
+      if (lane == 0) sched_release(k);
+      if (idx >= n_units) break;
+      const zp_attn_item it = args.items[kPair ? 2 * idx + int(cta) : idx];
       TileCursor cur(args.segs, it.seg_begin, it.seg_count, it.q_pos0 + it.q_len - 1);
       if (count_tiles(args.segs, it) == 0) continue;
       const bool resume = (it.flags & ZP_ITEM_LOAD_STATE) != 0;
@@ -417,6 +536,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; cur.next(); ++j, ++jg) {
         mbar_wait(bar(B_SFULL + t), jg & 1);
         tc_fence_after();
+        const int tr = (lane == 0 && quad == 0 && jg < 256) ? t * 1280 + int(jg) * 5 : -1;
+        ZP_STAMP(tr);
         float s[128];
         {
           uint32_t r0[32], r1[32], r2[32], r3[32];
@@ -425,6 +546,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32(tS + 64, r2);
           tmem_ld32(tS + 96, r3);
           tmem_wait_ld();
+          ZP_STAMP(tr < 0 ? -1 : tr + 1);
 #pragma unroll
           for (int v = 0; v < 32; ++v) {
             s[v] = __uint_as_float(r0[v]);
@@ -442,14 +564,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < 128; ++c)
             if (c > lim) s[c] = -INFINITY;
         }
-        // row max with 3-input max (FMNMX3)
+        // row max with 3-input max (FMNMX3), four independent chains
         float mx0 = fmax3(s[0], s[1], s[2]), mx1 = fmax3(s[3], s[4], s[5]);
+        float mx2 = fmax3(s[6], s[7], s[8]), mx3 = fmax3(s[9], s[10], s[11]);
 #pragma unroll
-        for (int c = 6; c < 126; c += 4) {
+        for (int c = 12; c < 124; c += 8) {
           mx0 = fmax3(mx0, s[c], s[c + 1]);
           mx1 = fmax3(mx1, s[c + 2], s[c + 3]);
+          mx2 = fmax3(mx2, s[c + 4], s[c + 5]);
+          mx3 = fmax3(mx3, s[c + 6], s[c + 7]);
         }
-        const float mx = fmax3(mx0, mx1, fmaxf(s[126], s[127])) * sl2;
+        mx0 = fmax3(mx0, s[124], s[125]);
+        mx1 = fmax3(mx1, s[126], s[127]);
+        const float mx = fmax3(mx0, mx1, fmaxf(mx2, mx3)) * sl2;
+#ifdef ZP_TRACE
+        asm volatile("" ::"f"(mx));
+        ZP_STAMP(tr < 0 ? -1 : tr + 2);
+#endif
         // Lazy rescale: keep the reference max unless this tile exceeds it by
         // more than 2^8; P <= 256 is exact enough in bf16 / fp32 and O, l stay
         // consistent with the reference actually used.
@@ -457,19 +588,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float m_new = bump ? mx : m;
         const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
         const float alpha = bump ? ex2(m - m_use) : 1.f;
-        const float2 sl2x2 = make_float2(sl2, sl2);
-        const float2 negm = make_float2(-m_use, -m_use);
-        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
-        if (masked) {
-          exp_tile<false>(s, sl2x2, negm, tP, acc0, acc1);
-        } else {
-          exp_tile<true>(s, sl2x2, negm, tP, acc0, acc1);
-        }
-        const float2 acc = __fadd2_rn(acc0, acc1);
-        l = l * alpha + (acc.x + acc.y);
-        m = m_new;
-        // O_t must hold PV(g-1) before it is rescaled (and PV(g) follows this
-        // thread's arrival), so wait only when this warp actually rescales.
+        // O_t must hold PV(g-1) before it is rescaled, and PV(g) is issued only
+        // after this warp's first P arrival, so rescale first — and wait for
+        // PV(g-1) only when this warp actually rescales.
         if ((j > 0 || resume) && __any_sync(0xffffffffu, bump)) {
           if (j > 0) {
             mbar_wait(bar(B_ODONE + t), (jg - 1) & 1);
@@ -490,9 +611,33 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_st32(tO + c * 32, rr);
           }
         }
+        // P in two 64-key halves; the MMA issues PV over the first half while
+        // the second half's exponentials run.
+        const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m_use, -m_use);
+        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+        if (masked) exp_half<0, false>(s, sl2x2, negm, tP, acc0, acc1);
+        else exp_half<0, true>(s, sl2x2, negm, tP, acc0, acc1);
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(bar(B_PFULL + t));
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (kPair) mbar_arrive_remote(pfull);
+          else mbar_arrive(pfull);
+        }
+        ZP_STAMP(tr < 0 ? -1 : tr + 3);
+        if (masked) exp_half<1, false>(s, sl2x2, negm, tP, acc0, acc1);
+        else exp_half<1, true>(s, sl2x2, negm, tP, acc0, acc1);
+        const float2 acc = __fadd2_rn(acc0, acc1);
+        l = l * alpha + (acc.x + acc.y);
+        m = m_new;
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (kPair) mbar_arrive_remote(pfull + 8);
+          else mbar_arrive(pfull + 8);
+        }
+        ZP_STAMP(tr < 0 ? -1 : tr + 4);
       }
 
       // ---------------- epilogue of this item (overlaps the next item's S MMAs)
@@ -547,16 +692,101 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  __syncwarp();
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync_all();  // the peer's last MMAs / arrivals are done
+  else __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem, 512);
+  if (warp == 1) {
+    if constexpr (kPair) tmem_dealloc_pair(tmem, 512);
+    else tmem_dealloc(tmem, 512);
+  }
 }
 
 }  // namespace zp
 
 // ------------------------------------------------------------------ host side
 #include "zp_host.h"
+
+namespace {
+
+// ZP_ATTN_VARIANT=single forces the one-CTA kernel (A/B measurements).
+bool pair_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("ZP_ATTN_VARIANT");
+    v = (e && e[0] == 's') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+template <bool kPair>
+int launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, zp::AttnArgs a,
+                int n_units, cudaStream_t stream) {
+  using namespace zp;
+  constexpr uint32_t smem = Cfg<kPair>::kSmemBytes;
+  static bool attr_done = false;
+  static int max_units = 0;  // resident CTAs (single) or CTA pairs (pair)
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem));
+    if (e != cudaSuccess) return zp_fail_cuda(e, "zp_attn_fwd: smem attribute");
+    const int sms = zp_device_sm_count();
+    if (sms <= 0) return zp_fail(ZP_ENODEV, "zp_attn_fwd: cannot query SM count");
+    max_units = sms;
+    if (kPair) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(2 * (sms / 2));
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int clusters = 0;
+      e = cudaOccupancyMaxActiveClusters(&clusters, attn_fwd_kernel<kPair>, &cfg);
+      if (e != cudaSuccess || clusters <= 0) {
+        cudaGetLastError();
+        clusters = sms / 2;
+      }
+      max_units = clusters;
+    }
+    attr_done = true;
+  }
+  a.n_units = n_units;
+  const int units = n_units < max_units ? n_units : max_units;  // persistent
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  if (kPair) {
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(2 * units);
+  } else {
+    cfg.gridDim = dim3(units);
+  }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, attn_fwd_kernel<kPair>, tq, tk, tv, a);
+  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_attn_fwd: launch");
+  return ZP_OK;
+}
+
+}  // namespace
+
+#ifdef ZP_TRACE
+extern "C" ZP_API int zp_debug_trace(unsigned long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, zp::g_zp_trace, sizeof(unsigned long long) * (n < 4096 ? n : 4096)) ==
+                 cudaSuccess ? 0 : -1;
+}
+#endif
 
 extern "C" int zp_attn_fwd(const void* q, const void* k, const void* v, int q_rows, int kv_rows,
                            int kv_row_stride, int hq, int hkv, int head_dim, void* o, float* lse,
@@ -575,29 +805,24 @@ extern "C" int zp_attn_fwd(const void* q, const void* k, const void* v, int q_ro
     return zp_fail(ZP_EINVAL, "zp_attn_fwd: null pointer");
   if (zp_check_device() != ZP_OK) return ZP_ENODEV;
 
+  // CTA pairs need both head pairs of a pair item to share the KV head
+  // (GQA group a multiple of 4) and the item list in aligned pairs.
+  const bool pair = (hq / hkv) % 4 == 0 && n_items % 2 == 0 && !pair_disabled();
   CUtensorMap tq, tk, tv;
   int rc;
   if ((rc = zp_make_tmap_2d_bf16(&tq, q, uint64_t(hq) * kHeadDim, uint64_t(q_rows),
                                  uint64_t(hq) * kHeadDim * 2, 64, 128)) != ZP_OK)
     return rc;
   if ((rc = zp_make_tmap_2d_bf16(&tk, k, uint64_t(hkv) * kHeadDim, uint64_t(kv_rows),
-                                 uint64_t(kv_row_stride) * 2, 64, 128)) != ZP_OK)
+                                 uint64_t(kv_row_stride) * 2, 64, pair ? 64 : 128)) != ZP_OK)
     return rc;
   if ((rc = zp_make_tmap_2d_bf16(&tv, v, uint64_t(hkv) * kHeadDim, uint64_t(kv_rows),
                                  uint64_t(kv_row_stride) * 2, 64, 128)) != ZP_OK)
     return rc;
 
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kSmemBytes));
-    if (e != cudaSuccess) return zp_fail_cuda(e, "zp_attn_fwd: smem attribute");
-    attr_done = true;
-  }
   AttnArgs a;
   a.items = items;
-  a.n_items = n_items;
-  a.next_item = reinterpret_cast<int*>(workspace);
+  a.next_unit = reinterpret_cast<int*>(workspace);
   a.segs = segs;
   a.o = reinterpret_cast<__nv_bfloat16*>(o);
   a.lse = lse;
@@ -608,15 +833,9 @@ extern "C" int zp_attn_fwd(const void* q, const void* k, const void* v, int q_ro
   a.hq = hq;
   a.group = hq / hkv;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
-  static int sms = 0;
-  if (sms == 0) sms = zp_device_sm_count();
-  if (sms <= 0) return zp_fail(ZP_ENODEV, "zp_attn_fwd: cannot query SM count");
-  const int grid = n_items < sms ? n_items : sms;  // persistent: one CTA per SM
-  cudaError_t me = cudaMemsetAsync(workspace, 0, sizeof(int), reinterpret_cast<cudaStream_t>(stream));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t me = cudaMemsetAsync(workspace, 0, sizeof(int), s);
   if (me != cudaSuccess) return zp_fail_cuda(me, "zp_attn_fwd: workspace reset");
-  attn_fwd_kernel<<<grid, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(
-      tq, tk, tv, a);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_attn_fwd: launch");
-  return ZP_OK;
+  return pair ? launch_attn<true>(tq, tk, tv, a, n_items / 2, s)
+              : launch_attn<false>(tq, tk, tv, a, n_items, s);
 }
