@@ -93,6 +93,46 @@ ZP_API int zp_attn_fwd(const void* q, const void* k, const void* v, int q_rows, 
                 float* state_o, float* state_ml, int state_rows, float softmax_scale,
                 void* workspace, void* stream);
 
+/* ---------------------------------------------------------------- backward
+ * (the reference charges backward as a multiple of the
+ * forward, topology.py:37 / simulator.py:304; executed here for the same
+ * LocalTask and RingRound work, attention_engine.py:229-265.)
+ *
+ * One backward work item: up to 128 keys (rows [kv_row0, +kv_len) of k/v,
+ * global positions [kv_pos0, ...)) of KV head kv_head, against every query of
+ * the query segments [qseg_begin, +qseg_count) (zp_kv_seg rows/positions of
+ * q) that can see them, for all hq/hkv query heads of the group. */
+typedef struct zp_bwd_item {
+  int32_t kv_row0;
+  int32_t kv_pos0;
+  int32_t kv_len;     /* 1..128 */
+  int32_t kv_head;
+  int32_t qseg_begin;
+  int32_t qseg_count;
+  int32_t flags;      /* ZP_BWD_* */
+  int32_t reserved;
+} zp_bwd_item;
+
+#define ZP_BWD_ACCUMULATE 1 /* add dK/dV into dk/dv instead of overwriting */
+
+/* delta[h * delta_stride + row] = sum_d o[row,h,d] * dout[row,h,d] (fp32);
+ * o, dout: [rows, hq, 128] bf16. */
+ZP_API int zp_attn_bwd_prep(const void* o, const void* dout, int rows, int hq, int head_dim,
+                     float* delta, int delta_stride, void* stream);
+
+/* Causal flash attention backward over a work-item list (bf16 in, fp32
+ * accumulate).  q, dout: [q_rows, hq, 128] bf16 (row-contiguous); k, v as in
+ * zp_attn_fwd; lse (natural log, the forward's FINAL value) and delta:
+ * [hq, lse_stride] fp32.  dq: [q_rows, hq, 128] fp32, ACCUMULATED with
+ * atomic adds (zero it before the first call); dk, dv: [kv_rows, hkv, 128]
+ * fp32, each item writes (or, with ZP_BWD_ACCUMULATE, adds to) its own rows —
+ * items of one call must cover disjoint (key row, kv head) tiles. */
+ZP_API int zp_attn_bwd(const void* q, const void* k, const void* v, const void* dout, int q_rows,
+                int kv_rows, int kv_row_stride, int hq, int hkv, int head_dim, const float* lse,
+                const float* delta, int lse_stride, float* dq, float* dk, float* dv,
+                const zp_bwd_item* items, int n_items, const zp_kv_seg* qsegs,
+                float softmax_scale, void* stream);
+
 /* Row-range copy with 16-byte vector loads/stores.  For each range i:
  * dst rows [dst_row0[i], +n_rows[i]) <- src rows [src_row0[i], +n_rows[i]).
  * ranges: device int32 [n_ranges][3] = {dst_row0, src_row0, n_rows}.

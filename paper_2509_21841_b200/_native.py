@@ -25,6 +25,9 @@ _c_int, _c_i64, _c_float, _vp = ctypes.c_int, ctypes.c_int64, ctypes.c_float, ct
 SIGNATURES: dict[str, tuple] = {
     "zp_attn_fwd": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                              _vp, _vp, _c_int, _vp, _c_int, _vp, _vp, _vp, _c_int, _c_float, _vp, _vp]),
+    "zp_attn_bwd_prep": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _vp, _c_int, _vp]),
+    "zp_attn_bwd": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp,
+                             _c_int, _vp, _vp, _vp, _vp, _c_int, _vp, _c_float, _vp]),
     "zp_copy_rows": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_i64, _vp, _c_int, _c_int, _vp]),
     "zp_remap_push": (_c_int, [_vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                ctypes.c_int32, _c_int, _vp]),

@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .worklist import QueryFragment, WorkList, build_worklist
+from .worklist import BwdWorkList, QueryFragment, WorkList, build_bwd_worklist, build_worklist
 
 HEAD_DIM = 128
 
@@ -112,6 +112,73 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, items: torch.Ten
     if _hook is not None:
         ev1.record()
         _hook("zp_attn_fwd", ev0, ev1)
+
+
+def upload_bwd_worklist(wl: BwdWorkList, device: torch.device) -> tuple[torch.Tensor, torch.Tensor]:
+    items = torch.from_numpy(wl.items.view(np.int32).reshape(-1)).pin_memory().to(device, non_blocking=True)
+    qsegs = torch.from_numpy(wl.qsegs.view(np.int32).reshape(-1)).pin_memory().to(device, non_blocking=True)
+    return items, qsegs
+
+
+def attn_bwd_prep(o: torch.Tensor, dout: torch.Tensor, delta: torch.Tensor,
+                  stream: torch.cuda.Stream | None = None) -> None:
+    """delta [Hq, >=T] fp32 <- rowsum(dO * O) per (head, row) (zp_attn_bwd_prep)."""
+    _require_cuda(o, dout, delta)
+    t, hq, d = o.shape
+    if dout.shape != o.shape or o.dtype != torch.bfloat16 or dout.dtype != torch.bfloat16:
+        raise ValueError("o and dout must be bf16 tensors of equal shape")
+    if not (o.is_contiguous() and dout.is_contiguous()) or delta.dtype != torch.float32 or delta.shape[0] != hq:
+        raise ValueError("o/dout must be contiguous, delta fp32 [Hq, >=T]")
+    _count_launch()
+    _native.call("zp_attn_bwd_prep", o.data_ptr(), dout.data_ptr(), t, hq, d, delta.data_ptr(),
+                 delta.stride(0), _stream_ptr(stream))
+
+
+def attn_bwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, dout: torch.Tensor, lse: torch.Tensor,
+             delta: torch.Tensor, dq: torch.Tensor, dk: torch.Tensor, dv: torch.Tensor, items: torch.Tensor,
+             n_items: int, qsegs: torch.Tensor, softmax_scale: float | None = None,
+             stream: torch.cuda.Stream | None = None) -> None:
+    """Launch zp_attn_bwd over a device backward work list.
+
+    q/dout [Tq, Hq, 128] bf16; k/v [Tk, Hkv, 128] bf16 (row stride may exceed
+    Hkv*128); lse/delta fp32 [Hq, >=Tq]; dq fp32 [Tq, Hq, 128] (accumulated),
+    dk/dv fp32 [Tk, Hkv, 128] contiguous."""
+    _require_cuda(q, k, v, dout, lse, delta, dq, dk, dv)
+    tq, hq, d = q.shape
+    tk, hkv, _ = k.shape
+    if dout.shape != q.shape or not dout.is_contiguous() or q.stride() != (hq * d, d, 1):
+        raise ValueError("q and dout must be row-contiguous [T, H, 128] of equal shape")
+    if k.stride()[1:] != (d, 1) or v.stride() != k.stride() or v.shape != k.shape:
+        raise ValueError("k/v must have contiguous heads and equal strides")
+    for t_, shape in ((dq, q.shape), (dk, k.shape), (dv, k.shape)):
+        if t_.dtype != torch.float32 or t_.shape != shape or not t_.is_contiguous():
+            raise ValueError("dq/dk/dv must be contiguous fp32 with the q/k shapes")
+    if lse.stride() != delta.stride() or lse.dtype != torch.float32 or delta.dtype != torch.float32:
+        raise ValueError("lse and delta must be fp32 with equal strides")
+    scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
+    _count_launch()
+    _native.call("zp_attn_bwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(), tq, tk, k.stride(0),
+                 hq, hkv, d, lse.data_ptr(), delta.data_ptr(), lse.stride(0), dq.data_ptr(), dk.data_ptr(),
+                 dv.data_ptr(), items.data_ptr(), n_items, qsegs.data_ptr(), scale, _stream_ptr(stream))
+
+
+def varlen_attention_backward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
+                              lse: torch.Tensor, dout: torch.Tensor, seqlens,
+                              softmax_scale: float | None = None):
+    """Backward of ``varlen_attention`` (LocalTask queue of one rank).
+    Returns (dq, dk, dv) bf16 in the input shapes."""
+    _require_cuda(q, k, v, o, lse, dout)
+    t, hq, d = q.shape
+    hkv = k.shape[1]
+    wl = build_bwd_worklist(local_fragments(seqlens), hkv)
+    delta = torch.empty_like(lse)
+    attn_bwd_prep(o, dout, delta)
+    dq = torch.zeros(q.shape, dtype=torch.float32, device=q.device)
+    dk = torch.zeros(k.shape, dtype=torch.float32, device=q.device)
+    dv = torch.zeros(k.shape, dtype=torch.float32, device=q.device)
+    items, qsegs = upload_bwd_worklist(wl, q.device)
+    attn_bwd(q, k, v, dout, lse, delta, dq, dk, dv, items, wl.n_items, qsegs, softmax_scale)
+    return dq.to(torch.bfloat16), dk.to(torch.bfloat16), dv.to(torch.bfloat16)
 
 
 def local_fragments(seqlens: list[int] | np.ndarray, row0: int = 0) -> list[QueryFragment]:

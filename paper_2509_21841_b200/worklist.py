@@ -138,3 +138,102 @@ def build_worklist(frags: list[QueryFragment], n_head_pairs: int,
     items["head_pair"] = np.tile(np.arange(n_head_pairs), n_tiles)
     kv_tiles = int(tiles["cost"].sum()) * n_head_pairs
     return WorkList(items, segs, pairs, kv_tiles)
+
+
+# ------------------------------------------------------------------ backward
+
+BWD_ITEM_DTYPE = np.dtype([("kv_row0", "<i4"), ("kv_pos0", "<i4"), ("kv_len", "<i4"), ("kv_head", "<i4"),
+                           ("qseg_begin", "<i4"), ("qseg_count", "<i4"), ("flags", "<i4"),
+                           ("reserved", "<i4")])
+BWD_ACCUMULATE = 1
+BWD_QBLOCK = 64
+
+
+def kv_tile_visible_pairs(kv_pos0: np.ndarray, kv_len: np.ndarray, qsegs: list[tuple[int, int, int]]) -> np.ndarray:
+    """Exact visible (q,k) pairs of key tiles [kv_pos0, +kv_len) against query
+    segments (row0, pos0, len) of the same sequence (key position <= query
+    position, reference attention_engine.py:113-136), vectorised over tiles."""
+    c = kv_pos0.astype(np.int64)
+    d = c + kv_len.astype(np.int64)  # keys [c, d)
+    total = np.zeros_like(c)
+    for _, a, m in qsegs:
+        if m <= 0:
+            continue
+        b = a + m  # queries [a, b)
+        # key p sees b - max(a, p) queries when p < b: keys [c, min(d, a+1)) see m each,
+        # keys [max(c, a+1), min(d, b)) see b - p
+        lo_full = np.minimum(d, a + 1)
+        total += np.maximum(lo_full - c, 0) * m
+        lo = np.maximum(c, a + 1)
+        hi = np.minimum(d, b)  # exclusive
+        n = np.maximum(hi - lo, 0)
+        total += np.where(n > 0, ((b - lo) + (b - hi + 1)) * n // 2, 0)
+    return total
+
+
+@dataclass
+class BwdWorkList:
+    items: np.ndarray      # BWD_ITEM_DTYPE, longest-first
+    qsegs: np.ndarray      # SEG_DTYPE
+    pairs_per_head: int    # visible causal pairs for one query head
+    steps: int             # query-block steps summed over items (per GQA group member)
+
+    @property
+    def n_items(self) -> int:
+        return int(self.items.shape[0])
+
+
+def build_bwd_worklist(frags: list[QueryFragment], n_kv_heads: int, flags: int = BWD_ACCUMULATE) -> BwdWorkList:
+    """Backward work items (``zp_attn_bwd``): every 128-key tile of every KV
+    segment the fragments attend to, once per KV head, with the list of query
+    fragments that see it.  Fragments sharing a KV segment (the zigzag ranges
+    of one sequence in a ring round) are grouped so items cover disjoint key
+    tiles."""
+    by_seg: dict[tuple[int, int, int], list[tuple[int, int, int]]] = {}
+    for f in frags:
+        if f.length <= 0:
+            continue
+        for seg in f.segs:
+            if seg[2] > 0:
+                by_seg.setdefault(tuple(seg), []).append((f.row0, f.pos0, f.length))
+    qrows: list[tuple[int, int, int, int]] = []
+    cols = {k: [] for k in ("kv_row0", "kv_pos0", "kv_len", "qseg_begin", "qseg_count", "cost")}
+    pairs = 0
+    for (r0, p0, ln), qs in sorted(by_seg.items()):
+        offs = np.arange(0, ln, TILE, dtype=np.int64)
+        kl = np.minimum(TILE, ln - offs)
+        kp = p0 + offs
+        vis = kv_tile_visible_pairs(kp, kl, qs)
+        keep = vis > 0
+        if not keep.any():
+            continue
+        pairs += int(vis[keep].sum())
+        begin = len(qrows)
+        qrows.extend((a, b, c, 0) for a, b, c in qs)
+        # cost: query blocks the kernel walks for each tile
+        cost = np.zeros_like(kp)
+        for _, a, m in qs:
+            first = np.where(kp > a, (kp - a) // BWD_QBLOCK, 0)
+            nb = (m + BWD_QBLOCK - 1) // BWD_QBLOCK
+            cost += np.where(a + m - 1 >= kp, nb - first, 0)
+        k = int(keep.sum())
+        cols["kv_row0"].append(r0 + offs[keep])
+        cols["kv_pos0"].append(kp[keep])
+        cols["kv_len"].append(kl[keep])
+        cols["qseg_begin"].append(np.full(k, begin))
+        cols["qseg_count"].append(np.full(k, len(qs)))
+        cols["cost"].append(cost[keep])
+    qsegs = np.zeros(max(len(qrows), 1), dtype=SEG_DTYPE)
+    for i, row in enumerate(qrows):
+        qsegs[i] = row
+    if not cols["kv_row0"]:
+        return BwdWorkList(np.zeros(0, dtype=BWD_ITEM_DTYPE), qsegs, 0, 0)
+    tiles = {k: np.concatenate(v) for k, v in cols.items()}
+    order = np.argsort(-tiles["cost"], kind="stable")
+    n_tiles = order.shape[0]
+    items = np.zeros(n_tiles * n_kv_heads, dtype=BWD_ITEM_DTYPE)
+    for name in ("kv_row0", "kv_pos0", "kv_len", "qseg_begin", "qseg_count"):
+        items[name] = np.repeat(tiles[name][order], n_kv_heads)
+    items["kv_head"] = np.tile(np.arange(n_kv_heads), n_tiles)
+    items["flags"] = flags
+    return BwdWorkList(items, qsegs, pairs, int(tiles["cost"].sum()) * n_kv_heads)
