@@ -63,3 +63,54 @@ def run_items(items, segs, q, k, v, o, lse, state, scale):
                 with np.errstate(invalid="ignore", divide="ignore"):
                     o[r0:r0 + n, h, :] = np.where(l_new[:, None] > 0, o_new / l_new[:, None], 0.0)
                     lse[h, r0:r0 + n] = np.where(l_new > 0, m_use + np.log(l_new), -np.inf)
+
+
+def run_bwd_items(items, qsegs, q, k, v, dout, lse, delta, scale, qblock=64):
+    """Execute backward work items (zp_bwd_item, include/zeppelin_b200.h) in
+    float64 exactly as documented: every 128-key tile against the 64-row
+    query blocks of its query segments from the first block that can see the
+    tile's first key, all query heads of the GQA group, mask k_pos <= q_pos.
+    lse [Hq, Tq] (natural log) and delta [Hq, Tq] = rowsum(dO * O) come from
+    the forward.  Returns (dq, dk, dv, pairs_per_head) with dk/dv written per item (the
+    ACCUMULATE flag adds)."""
+    hq, d = q.shape[1], q.shape[2]
+    hkv = k.shape[1]
+    grp = hq // hkv
+    dq = np.zeros(q.shape)
+    dk = np.zeros(k.shape)
+    dv = np.zeros(k.shape)
+    pairs = 0
+    for it in items:
+        kr0, kp0, kn, g = (int(it[x]) for x in ("kv_row0", "kv_pos0", "kv_len", "kv_head"))
+        kpos = kp0 + np.arange(kn)
+        gk = np.zeros((kn, d))
+        gv = np.zeros((kn, d))
+        for s in qsegs[int(it["qseg_begin"]): int(it["qseg_begin"]) + int(it["qseg_count"])]:
+            r0, p0, n = int(s["row0"]), int(s["pos0"]), int(s["len"])
+            if n <= 0 or p0 + n - 1 < kp0:
+                continue
+            b0 = max(0, (kp0 - p0) // qblock) if kp0 > p0 else 0
+            rows = np.arange(b0 * qblock, n)
+            qpos = p0 + rows
+            vis = kpos[None, :] <= qpos[:, None]
+            if g == 0:
+                pairs += int(vis.sum())
+            for h in range(g * grp, (g + 1) * grp):
+                qq = q[r0 + rows, h, :]
+                kk = k[kr0:kr0 + kn, g, :]
+                vv = v[kr0:kr0 + kn, g, :]
+                do = dout[r0 + rows, h, :]
+                p = np.where(vis, np.exp(qq @ kk.T * scale - lse[h, r0 + rows][:, None]), 0.0)
+                dp = do @ vv.T
+                ds = p * (dp - delta[h, r0 + rows][:, None])
+                gv += p.T @ do
+                gk += ds.T @ qq * scale
+                dq[r0 + rows, h, :] += ds @ kk * scale
+        acc = int(it["flags"]) & 1
+        if acc:
+            dk[kr0:kr0 + kn, g] += gk
+            dv[kr0:kr0 + kn, g] += gv
+        else:
+            dk[kr0:kr0 + kn, g] = gk
+            dv[kr0:kr0 + kn, g] = gv
+    return dq, dk, dv, pairs

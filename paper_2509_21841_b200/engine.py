@@ -13,6 +13,12 @@ Public entry points (drop-in execution of what the reference only costs):
   attention for this rank (reference simulator.py:124-188 charges it);
 * ``remap_forward(layout, x)`` / ``remap_inverse(layout, y)`` — the
   attention<->linear token remap (simulator.py:282-302, remapping.py:187-255);
+* ``attention_backward(plan, schedule, q, k, v, o, lse, dout)`` — its
+  backward: LocalTask + RingRound gradients, dK/dV of a
+  ring's KV sets travelling with them around the ring and returned to their
+  owner with one extra hop (the reference charges g sends, README.md:119-124);
+  the remap's backward is the transposed move (``remap_inverse`` /
+  ``remap_forward`` of the gradient, remapping.py:248-255);
 * ``ZeppelinLayer`` — plan + attention + remap for one batch.
 """
 
@@ -27,10 +33,10 @@ import torch.distributed as dist
 
 from . import ops
 from .plan import build_plan
-from .program import RankProgram, build_rank_program
+from .program import BwdProgram, RankProgram, build_bwd_program, build_rank_program
 from .remap import RemapLayout, remap_layout
 from .schedule import build_schedule
-from .worklist import WorkList
+from .worklist import BwdWorkList, WorkList
 
 
 class RankContext:
@@ -230,6 +236,119 @@ def attention_forward(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torch
     for rp, (pack, rounds) in zip(prog.rings, devp.rings):
         run(ctx, rp, pack, rounds, q, k, v, o, lse, scale)
     return o, lse
+
+
+# ------------------------------------------------------------------ backward
+
+class BwdDeviceProgram:
+    """A BwdProgram's int32 tables, uploaded with one pinned H2D copy."""
+
+    def __init__(self, bp: BwdProgram, device: torch.device):
+        self.bp = bp
+        chunks: list[np.ndarray] = []
+
+        def add(arr: np.ndarray) -> tuple[int, int]:
+            flat = np.ascontiguousarray(arr).view(np.int32).reshape(-1)
+            off = sum(c.size for c in chunks)
+            chunks.append(flat)
+            return off, flat.size
+
+        def add_work(wl: BwdWorkList):
+            return add(wl.items), add(wl.qsegs), wl.n_items
+
+        local = add_work(bp.local)
+        rings = [([add_work(wl) for wl in lists], add(up)) for lists, up in zip(bp.rounds, bp.unpack_ranges)]
+        host = np.concatenate(chunks) if chunks else np.zeros(1, np.int32)
+        self.table = torch.from_numpy(host).pin_memory().to(device, non_blocking=True)
+
+        def view(span):
+            off, n = span
+            return self.table[off:off + n]
+
+        self.local = _DevWork(view(local[0]), view(local[1]), local[2])
+        self.rings = [([_DevWork(view(a), view(b), n) for a, b, n in rounds], view(up)) for rounds, up in rings]
+
+
+def _run_ring_backward(ctx: RankContext, rp, dev_pack, dev_rounds, dev_unpack, q, k, v, dout, lse, delta,
+                       dq, dk, dv, scale):
+    """Ring backward: round r computes dQ (accumulated in place) and the
+    contribution of this rank's queries to dK/dV of the KV set it holds; the
+    partial dK/dV travel with the KV set to position i+1, and after the last
+    round one more hop returns every set's gradient to its owner."""
+    hkv, d = k.shape[1], k.shape[2]
+    g = rp.group_size
+    rows = max(rp.held_rows)
+    kv = [ctx.workspace(f"ringkv{j}", (rows, 2, hkv, d), torch.bfloat16) for j in (0, 1)]
+    gk = [ctx.workspace(f"ringdk{j}", (rows, hkv, d), torch.float32) for j in (0, 1)]
+    gv = [ctx.workspace(f"ringdv{j}", (rows, hkv, d), torch.float32) for j in (0, 1)]
+    n_pack = rp.pack_ranges.shape[0]
+    max_pack = int(rp.pack_ranges[:, 2].max()) if n_pack else 0
+    ops.copy_rows(kv[0][:, 0], k, dev_pack, n_pack, max_pack)
+    ops.copy_rows(kv[0][:, 1], v, dev_pack, n_pack, max_pack)
+    gk[0].zero_()
+    gv[0].zero_()
+    for r in range(g):
+        cur, nxt = r % 2, (r + 1) % 2
+        n_kv = rp.rounds[r].kv_rows
+        work = dev_rounds[r]
+        with ctx.span("compute", "intra_node.attn_bwd",
+                      {"ring": rp.ring_index, "round": r, "pairs": rp.rounds[r].work.pairs_per_head}):
+            if work.n:
+                ops.attn_bwd(q, kv[cur][:n_kv, 0], kv[cur][:n_kv, 1], dout, lse, delta, dq, gk[cur][:n_kv],
+                             gv[cur][:n_kv], work.items, work.n, work.segs, softmax_scale=scale)
+        # forward the KV set (not after the last round) and its gradient (always)
+        n_send, n_recv = rp.send_rows(r), rp.recv_rows(r)
+        p2p = []
+        with ctx.span("intra-comm", "dkv.send", {"ring": rp.ring_index, "round": r, "tokens": n_send,
+                                                  "dst": rp.next_rank}):
+            if n_send:
+                if r < g - 1:
+                    p2p.append(dist.P2POp(dist.isend, kv[cur][:n_send], rp.next_rank, ctx.group))
+                p2p += [dist.P2POp(dist.isend, gk[cur][:n_send], rp.next_rank, ctx.group),
+                        dist.P2POp(dist.isend, gv[cur][:n_send], rp.next_rank, ctx.group)]
+            if n_recv:
+                if r < g - 1:
+                    p2p.append(dist.P2POp(dist.irecv, kv[nxt][:n_recv], rp.prev_rank, ctx.group))
+                p2p += [dist.P2POp(dist.irecv, gk[nxt][:n_recv], rp.prev_rank, ctx.group),
+                        dist.P2POp(dist.irecv, gv[nxt][:n_recv], rp.prev_rank, ctx.group)]
+            if p2p:
+                for req in dist.batch_isend_irecv(p2p):
+                    req.wait()
+    own = g % 2  # buffer holding this rank's own set after the return hop
+    n_up = dev_unpack.numel() // 3
+    if n_up:
+        ops.copy_rows(dk, gk[own], dev_unpack, n_up, max_pack)
+        ops.copy_rows(dv, gv[own], dev_unpack, n_up, max_pack)
+
+
+def attention_backward(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
+                       lse: torch.Tensor, dout: torch.Tensor, ctx: RankContext | None = None,
+                       program: RankProgram | None = None, bwd_program: BwdDeviceProgram | None = None,
+                       softmax_scale: float | None = None):
+    """Gradients of this rank's attention (the backward of ``attention_forward``
+    with the same plan).  o / lse are the forward outputs (final LSE).
+    Returns (dq, dk, dv) bf16 in the rank's attention layout."""
+    ctx = ctx or RankContext.from_env()
+    hq, hkv = q.shape[1], k.shape[1]
+    prog = program or build_rank_program(plan, schedule, ctx.rank, hq)
+    if q.shape[0] != prog.rows or dout.shape != q.shape:
+        raise ValueError(f"rank {ctx.rank}: expected {prog.rows} attention-layout rows")
+    bdev = bwd_program or BwdDeviceProgram(build_bwd_program(prog, hkv), q.device)
+    scale = 1.0 / math.sqrt(q.shape[2]) if softmax_scale is None else softmax_scale
+    delta = torch.empty_like(lse)
+    ops.attn_bwd_prep(o, dout, delta)
+    dq = torch.zeros(q.shape, dtype=torch.float32, device=q.device)
+    dk = torch.zeros(k.shape, dtype=torch.float32, device=q.device)
+    dv = torch.zeros(k.shape, dtype=torch.float32, device=q.device)
+    if bdev.local.n:
+        with ctx.span("compute", "local.attn_bwd", {"pairs": bdev.bp.local.pairs_per_head}):
+            ops.attn_bwd(q, k, v, dout, lse, delta, dq, dk, dv, bdev.local.items, bdev.local.n, bdev.local.segs,
+                         softmax_scale=scale)
+    devp = DeviceProgram(prog, q.device) if prog.rings else None
+    for i, rp in enumerate(prog.rings):
+        rounds, unpack = bdev.rings[i]
+        _run_ring_backward(ctx, rp, devp.rings[i][0], rounds, unpack, q, k, v, dout, lse, delta, dq, dk, dv, scale)
+    return dq.to(torch.bfloat16), dk.to(torch.bfloat16), dv.to(torch.bfloat16)
 
 
 # ------------------------------------------------------------------ remap

@@ -27,8 +27,8 @@ import numpy as np
 
 from .remap import RemapLayout, remap_layout
 from .schedule import LOCAL, AttentionSchedule, RingSchedule, ring_source
-from .worklist import (ITEM_LOAD_STATE, ITEM_STORE_STATE, QueryFragment, WorkList, build_worklist,
-                       tile_visible_pairs, TILE)
+from .worklist import (ITEM_LOAD_STATE, ITEM_STORE_STATE, BwdWorkList, QueryFragment, WorkList,
+                       build_bwd_worklist, build_worklist, tile_visible_pairs, TILE)
 
 
 @dataclass
@@ -37,6 +37,7 @@ class RingRoundProgram:
     src_position: int
     kv_rows: int            # rows of the KV set held this round
     work: WorkList
+    frags: list[QueryFragment] = field(default_factory=list)  # query fragments vs the held KV
 
 
 @dataclass
@@ -74,6 +75,7 @@ class RankProgram:
     rings: list[RingProgram]
     remap: RemapLayout
     n_head_pairs: int
+    local_frags: list[QueryFragment] = field(default_factory=list)
 
     @property
     def max_held_rows(self) -> int:
@@ -172,7 +174,8 @@ def build_rank_program(plan, schedule: AttentionSchedule, rank: int, n_heads: in
             if wl.pairs_per_head != expect:
                 raise AssertionError(f"rank {rank} ring {ring.members} round {r}: work list covers "
                                      f"{wl.pairs_per_head} pairs, schedule says {expect}")
-            prog.rounds.append(RingRoundProgram(round_index=r, src_position=src, kv_rows=held[src], work=wl))
+            prog.rounds.append(RingRoundProgram(round_index=r, src_position=src, kv_rows=held[src], work=wl,
+                                                frags=frags))
         rings.append(prog)
 
     if remap is None:
@@ -180,4 +183,34 @@ def build_rank_program(plan, schedule: AttentionSchedule, rank: int, n_heads: in
     elif not isinstance(remap, RemapLayout):
         remap = remap_layout(plan.tokens_per_rank, remap)
     return RankProgram(rank=rank, world=plan.num_ranks, rows=at, frag_rows=frag_rows, local=local,
-                       rings=rings, remap=remap, n_head_pairs=n_hp)
+                       rings=rings, remap=remap, n_head_pairs=n_hp, local_frags=local_frags)
+
+
+@dataclass
+class BwdProgram:
+    """Backward work lists of a RankProgram (``zp_attn_bwd``): the LocalTask
+    list and one list per ring round, each covering exactly the forward's
+    visible pairs (checked), plus the row tables that return a ring's dK/dV
+    from its KV buffer to the attention layout."""
+    local: BwdWorkList
+    rounds: list[list[BwdWorkList]]      # [ring][round]
+    unpack_ranges: list[np.ndarray]      # [ring]: int32 [n, 3] (layout_row, buf_row, n_rows)
+
+
+def build_bwd_program(prog: RankProgram, n_kv_heads: int) -> BwdProgram:
+    local = build_bwd_worklist(prog.local_frags, n_kv_heads)
+    if local.pairs_per_head != prog.local.pairs_per_head:
+        raise AssertionError(f"rank {prog.rank}: backward local list covers {local.pairs_per_head} pairs, "
+                             f"forward {prog.local.pairs_per_head}")
+    rounds = []
+    for rp in prog.rings:
+        lists = []
+        for rr in rp.rounds:
+            wl = build_bwd_worklist(rr.frags, n_kv_heads)
+            if wl.pairs_per_head != rr.work.pairs_per_head:
+                raise AssertionError(f"rank {prog.rank} ring {rp.members} round {rr.round_index}: backward list "
+                                     f"covers {wl.pairs_per_head} pairs, forward {rr.work.pairs_per_head}")
+            lists.append(wl)
+        rounds.append(lists)
+    unpack = [np.ascontiguousarray(rp.pack_ranges[:, [1, 0, 2]]) for rp in prog.rings]
+    return BwdProgram(local=local, rounds=rounds, unpack_ranges=unpack)

@@ -188,3 +188,59 @@ def test_comparison_strategies_execute_exactly():
     for rank, errs in res.items():
         for strategy, err in errs.items():
             assert err <= 2e-2, (rank, strategy, err)
+
+
+def _backward_worker(rank, world, port, lengths, results):
+    import torch.distributed as dist
+    from paper_2509_21841_b200 import engine, plan as P, schedule as S
+    from paper_2509_21841_b200.batch import SequenceBatch
+    from paper_2509_21841_b200.cluster import single_box
+    from paper_2509_21841_b200.emulate import gather_rank
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        batch = SequenceBatch(tuple(enumerate(lengths)))
+        plan = P.build_plan(batch, single_box(world, batch.total_tokens))
+        sched = S.build_schedule(plan)
+        g = torch.Generator().manual_seed(4)
+        seqs = sorted(plan.sequence_lengths.items())
+        mk = lambda h: {s: torch.randn(n, h, 128, generator=g).to(torch.bfloat16) for s, n in seqs}  # noqa: E731
+        sq, sk, sv, sdo = mk(32), mk(8), mk(8), mk(32)
+        ctx = engine.RankContext(rank, world)
+        q, k, v, do = (gather_rank(x, plan, rank, "cuda") for x in (sq, sk, sv, sdo))
+        o, lse = engine.attention_forward(plan, sched, q, k, v, ctx)
+        dq, dk, dv = engine.attention_backward(plan, sched, q, k, v, o, lse, do, ctx)
+        torch.cuda.synchronize()
+        # fp32 autograd of whole sequences, sliced to this rank's fragments
+        ref = {}
+        for s, n in seqs:
+            qf, kf, vf = (t[s].float().cuda().requires_grad_(True) for t in (sq, sk, sv))
+            out = torch.nn.functional.scaled_dot_product_attention(
+                qf.transpose(0, 1), kf.repeat_interleave(4, 1).transpose(0, 1),
+                vf.repeat_interleave(4, 1).transpose(0, 1), is_causal=True).transpose(0, 1)
+            out.backward(sdo[s].float().cuda())
+            ref[s] = (qf.grad, kf.grad, vf.grad)
+        worst = 0.0
+        for j, got in enumerate((dq, dk, dv)):
+            want = torch.cat([ref[f.sequence_id][j][f.start:f.end] for f in plan.fragments[rank]])
+            err = (got.float() - want).abs().max().item()
+            worst = max(worst, err / (want.abs().max().item() + 1e-6))
+        results[rank] = (worst, len(plan.ring_groups))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_multi_gpu_backward_with_ring_dkv_exchange():
+    world = min(torch.cuda.device_count(), 4)
+    lengths = [3000, 300, 1200, 40, 700]
+    with mp.Manager() as mgr:
+        res = mgr.dict()
+        mp.spawn(_backward_worker, args=(world, _port(), lengths, res), nprocs=world, join=True)
+        res = dict(res)
+    assert sorted(res) == list(range(world))
+    assert any(v[1] > 0 for v in res.values()), "config must exercise rings"
+    for rank, (rel, _) in res.items():
+        assert rel <= 2.5e-2, res
