@@ -586,6 +586,96 @@ def run_block(args):
         dist.destroy_process_group()
 
 
+def run_backward(args):
+    """one training step of the attention layer — forward
+    (LocalTask + ring rounds) and backward (zp_attn_bwd, ring dK/dV travelling
+    with the KV sets) — on the layer workload (C2 at N=1, C3 at N>1)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_21841_b200 import engine, ops
+    from paper_2509_21841_b200 import plan as P, schedule as S
+    from paper_2509_21841_b200.program import build_bwd_program, build_rank_program
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    ctx = engine.RankContext(rank, world, dev)
+    name, batch, cluster = workload(world)
+    hq, hkv, d = 32, 8, 128
+    plan = P.build_plan(batch, cluster)
+    sched = S.build_schedule(plan)
+    prog = build_rank_program(plan, sched, rank, hq)
+    devp = engine.DeviceProgram(prog, dev)
+    bdev = engine.BwdDeviceProgram(build_bwd_program(prog, hkv), dev)
+    rows = prog.rows
+    g = torch.Generator(device=dev).manual_seed(99 + rank)
+    q, dout = (torch.randn(rows, hq, d, device=dev, generator=g, dtype=torch.bfloat16) for _ in range(2))
+    k, v = (torch.randn(rows, hkv, d, device=dev, generator=g, dtype=torch.bfloat16) for _ in range(2))
+    events: list[tuple] = []
+
+    def step(record=False):
+        if record:
+            ops.set_launch_hook(lambda nm, a, b: events.append((nm, a, b)))
+        o, lse = engine.attention_forward(plan, sched, q, k, v, ctx, prog, devp)
+        engine.attention_backward(plan, sched, q, k, v, o, lse, dout, ctx, prog, bdev)
+        ops.set_launch_hook(None)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ops.reset_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        e0.record()
+        for _ in range(args.steps):
+            step(record=True)
+        e1.record()
+        torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    fwd_ms = sum(a.elapsed_time(b) for nm, a, b in events if nm == "zp_attn_fwd") / args.steps
+    bwd_ms = sum(a.elapsed_time(b) for nm, a, b in events if nm == "zp_attn_bwd") / args.steps
+    pairs = prog.pairs_per_head()
+    st = torch.tensor([float(pairs), fwd_ms, bwd_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        gathered = [torch.zeros_like(st) for _ in range(world)]
+        dist.all_gather(gathered, st)
+    else:
+        gathered = [st]
+    per = [x.tolist() for x in gathered]
+    busiest = max(range(world), key=lambda i: per[i][0])
+    peak, peak_sus, _, kind = _peaks()
+    bwd_flop = per[busiest][0] * 10 * 128 * 32
+    bwd_tf = bwd_flop / (per[busiest][2] / 1e3) / 1e12 if per[busiest][2] > 0 else 0.0
+    fwd_tf = per[busiest][0] * FLOP_PER_PAIR / (per[busiest][1] / 1e3) / 1e12 if per[busiest][1] > 0 else 0.0
+    line = {
+        "metric": "attention layer training step (fwd+bwd) tokens/s", "value": batch.total_tokens / (ms / 1e3),
+        "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded batch from the reference's length mixtures; N(0,1) q/k/v/dO)",
+        "config": {"workload": name, "total_tokens": batch.total_tokens, "rings": len(plan.ring_groups)},
+        "roofline": {"bound": "tensor", "kernel": "zp_attn_bwd (attn_bwd_kernel)", "achieved": bwd_tf,
+                     "peak": peak, "unit": "TFLOP/s", "frac": bwd_tf / peak,
+                     "flop_per_pair": 10 * 128 * 32, "rank": busiest, "bwd_ms_per_step": per[busiest][2],
+                     "fwd_ms_per_step": per[busiest][1], "fwd_tflops": fwd_tf,
+                     "peak_kind": f"{kind} burst bf16 (MEASURED_PEAKS.json)"},
+        "gpu_launches": ops.launch_count(), "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        emit(line)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_compare(args):
     """the paper's comparison executed, not modelled.  The
     same batch runs under zeppelin, te_cp, llama_cp and hybrid_dp plans
@@ -682,8 +772,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-remap-stress", action="store_true")
-    ap.add_argument("--workload", choices=["layer", "c5", "compare"], default="layer",
-                    help="layer: attn+remap (BASELINE metric); c5: full transformer block")
+    ap.add_argument("--workload", choices=["layer", "c5", "compare", "train"], default="layer",
+                    help="layer: attn+remap (BASELINE metric); c5: full transformer block; "
+                         "train: attention fwd+bwd step")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "zeppelin":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
@@ -693,6 +784,8 @@ def main():
         run_block(args)
     elif args.workload == "compare":
         run_compare(args)
+    elif args.workload == "train":
+        run_backward(args)
     else:
         run_gpu(args)
 

@@ -157,9 +157,15 @@ def attn_bwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, dout: torch.Tens
         raise ValueError("lse and delta must be fp32 with equal strides")
     scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
     _count_launch()
+    if _hook is not None:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
     _native.call("zp_attn_bwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(), tq, tk, k.stride(0),
                  hq, hkv, d, lse.data_ptr(), delta.data_ptr(), lse.stride(0), dq.data_ptr(), dk.data_ptr(),
                  dv.data_ptr(), items.data_ptr(), n_items, qsegs.data_ptr(), scale, _stream_ptr(stream))
+    if _hook is not None:
+        ev1.record()
+        _hook("zp_attn_bwd", ev0, ev1)
 
 
 def varlen_attention_backward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
