@@ -200,8 +200,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
+    {
+      // ---------------- MMA issuer (whole warp, warp-uniform operands; one
+      // elected lane issues each tcgen05 op)
       constexpr uint32_t idesc_t = idesc_bf16_f32(128, 64, 0, 0);    // S^T, dP^T
       constexpr uint32_t idesc_kv = idesc_bf16_f32(128, 128, 0, 1);  // dV, dK
       constexpr uint32_t idesc_q = idesc_bf16_f32(128, 64, 1, 1);    // dQ^T
@@ -233,15 +234,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kk = 0; kk < kD / 16; ++kk) {
           const uint64_t ao = ((kk >> 2) * kKVBox + (kk & 3) * 32) >> 4;
           const uint64_t bo = ((kk >> 2) * kQBox + (kk & 3) * 32) >> 4;
-          mma_ss(tS0 + 64 * buf, k_kmaj + ao, q_kmaj + q_step * buf + bo, idesc_t, kk > 0 ? 1u : 0u);
+          mma_ss_w(tS0 + 64 * buf, k_kmaj + ao, q_kmaj + q_step * buf + bo, idesc_t, kk > 0 ? 1u : 0u);
         }
 #pragma unroll 1
         for (int kk = 0; kk < kD / 16; ++kk) {
           const uint64_t ao = ((kk >> 2) * kKVBox + (kk & 3) * 32) >> 4;
           const uint64_t bo = ((kk >> 2) * kQBox + (kk & 3) * 32) >> 4;
-          mma_ss(tDP0 + 64 * buf, v_kmaj + ao, do_kmaj + q_step * buf + bo, idesc_t, kk > 0 ? 1u : 0u);
+          mma_ss_w(tDP0 + 64 * buf, v_kmaj + ao, do_kmaj + q_step * buf + bo, idesc_t, kk > 0 ? 1u : 0u);
         }
-        tc_commit(bar(B_SDP_FULL + buf));
+        tc_commit_w(bar(B_SDP_FULL + buf));
       };
       if (n_steps > 0) issue_sdp(0);
       for (int n = 0; n < n_steps; ++n) {
@@ -252,20 +253,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
         for (int kk = 0; kk < kBQ / 16; ++kk) {
           const uint32_t acc = (n > 0 || kk > 0) ? 1u : 0u;
-          mma_ss(tDV, pt_k + p_step * buf + ((kk * 32) >> 4), do_mn + q_step * buf + ((kk * 2048) >> 4),
+          mma_ss_w(tDV, pt_k + p_step * buf + ((kk * 32) >> 4), do_mn + q_step * buf + ((kk * 2048) >> 4),
                  idesc_kv, acc);
-          mma_ss(tDK, dst_k + p_step * buf + ((kk * 32) >> 4), q_mn + q_step * buf + ((kk * 2048) >> 4),
+          mma_ss_w(tDK, dst_k + p_step * buf + ((kk * 32) >> 4), q_mn + q_step * buf + ((kk * 2048) >> 4),
                  idesc_kv, acc);
         }
-        tc_commit(bar(B_QDO_EMPTY + buf));
+        tc_commit_w(bar(B_QDO_EMPTY + buf));
 #pragma unroll 1
         for (int kk = 0; kk < kBK / 16; ++kk)
-          mma_ss(tS0 + 64 * buf, k_mn + ((kk * 2048) >> 4), dst_mn + p_step * buf + ((kk * 2048) >> 4), idesc_q,
+          mma_ss_w(tS0 + 64 * buf, k_mn + ((kk * 2048) >> 4), dst_mn + p_step * buf + ((kk * 2048) >> 4), idesc_q,
                  kk > 0 ? 1u : 0u);
-        tc_commit(bar(B_DQ_FULL + buf));
-        tc_commit(bar(B_PDS_EMPTY + buf));
+        tc_commit_w(bar(B_DQ_FULL + buf));
+        tc_commit_w(bar(B_PDS_EMPTY + buf));
       }
-      tc_commit(bar(B_DKV));
+      tc_commit_w(bar(B_DKV));
     }
   } else if (warp >= 4 && warp < 8) {
     // ---------------- P^T / dS^T (thread == key row), then the dK / dV epilogue
