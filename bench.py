@@ -137,12 +137,14 @@ def run_gpu(args):
     name, batch, cluster = workload(world)
     hq, hkv, d = 32, 8, 128
 
+    stager = engine.TableStager(dev)
+
     def host_plan():
         plan = P.build_plan(batch, cluster)
         sched = S.build_schedule(plan)
         res = M.solve_remap(plan.tokens_per_rank, M.cost_matrix(cluster))
         prog = build_rank_program(plan, sched, rank, hq, res)
-        return plan, sched, prog, engine.DeviceProgram(prog, dev)
+        return plan, sched, prog, engine.DeviceProgram(prog, dev, stager)
 
     plan, sched, prog, devp = host_plan()
     rows = prog.rows

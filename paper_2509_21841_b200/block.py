@@ -123,10 +123,11 @@ class ZeppelinBlock:
             lay = identity_layout(self.plan.tokens_per_rank)
         self.schedule = build_schedule(self.plan)
         self.program = build_rank_program(self.plan, self.schedule, r, self.hq, lay)
-        self.device_program = engine.DeviceProgram(self.program, self.ctx.device)
+        if not hasattr(self, "_stagers"):
+            self._stagers = [engine.TableStager(self.ctx.device) for _ in range(2)]
+        self.device_program = engine.DeviceProgram(self.program, self.ctx.device, self._stagers[0])
         self.layout = self.program.remap
-        pos = attention_positions(self.plan, r)
-        self.pos = torch.from_numpy(pos).pin_memory().to(self.ctx.device, non_blocking=True)
+        self.pos = self._stagers[1].upload(np.ascontiguousarray(attention_positions(self.plan, r)))
         return self.plan
 
     @property

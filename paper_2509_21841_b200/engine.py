@@ -81,10 +81,59 @@ class _DevWork:
     n: int
 
 
+class TableStager:
+    """Reusable pinned staging + device buffers for per-step work-list uploads.
+
+    Allocating pinned memory every step (``tensor.pin_memory()``) and copying
+    on the compute stream ties the host to the device's progress and breaks
+    host-fed pipelines.  Here K slots rotate; each upload is a copy on a
+    private stream that waits only for the kernels that read the slot K
+    uploads ago (an event recorded on the compute stream at the next upload,
+    i.e. after those kernels were enqueued); the compute stream waits for the
+    copy.  The host blocks only if it runs K uploads ahead of the device."""
+
+    def __init__(self, device: torch.device, slots: int = 3):
+        self.device = device
+        self.slots = [None] * slots
+        self.turn = 0
+        self.prev = None
+        self.stream = torch.cuda.Stream(device)
+
+    def upload(self, host: np.ndarray) -> torch.Tensor:
+        cs = torch.cuda.current_stream(self.device)
+        if self.prev is not None:  # kernels reading the previous upload are enqueued by now
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            self.prev["consumed"] = ev
+        n = host.size
+        slot = self.slots[self.turn]
+        self.turn = (self.turn + 1) % len(self.slots)
+        if slot is None or slot["pin"].numel() < n:
+            cap = max(n, 1 << 16)
+            slot = {"pin": torch.empty(cap, dtype=torch.int32).pin_memory(),
+                    "dev": torch.empty(cap, dtype=torch.int32, device=self.device),
+                    "copied": None, "consumed": None}
+            self.slots[self.turn - 1] = slot
+        if slot["copied"] is not None:
+            slot["copied"].synchronize()  # the previous copy out of this pinned slot is done
+        slot["pin"][:n].numpy()[:] = host
+        dev = slot["dev"][:n]
+        with torch.cuda.stream(self.stream):
+            if slot["consumed"] is not None:
+                self.stream.wait_event(slot["consumed"])
+            dev.copy_(slot["pin"][:n], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(self.stream)
+        slot["copied"] = done
+        cs.wait_event(done)
+        self.prev = slot
+        return dev
+
+
 class DeviceProgram:
     """A RankProgram's int32 tables, uploaded with one pinned H2D copy."""
 
-    def __init__(self, prog: RankProgram, device: torch.device):
+    def __init__(self, prog: RankProgram, device: torch.device, stager: TableStager | None = None):
         self.prog = prog
         chunks: list[np.ndarray] = []
 
@@ -104,7 +153,10 @@ class DeviceProgram:
             rounds = [add_work(rr.work) for rr in rp.rounds]
             rings.append((pack, rounds))
         host = np.concatenate(chunks) if chunks else np.zeros(1, np.int32)
-        self.table = torch.from_numpy(host).pin_memory().to(device, non_blocking=True)
+        if stager is not None:
+            self.table = stager.upload(host)
+        else:
+            self.table = torch.from_numpy(host).pin_memory().to(device, non_blocking=True)
 
         def view(span):
             off, n = span
@@ -528,7 +580,8 @@ def remap_push(layout: RemapLayout, x: torch.Tensor, peer: PeerBuffer, ctx: Rank
     return out
 
 
-def pull_tables(layout: RemapLayout, rank: int, inverse: bool, device) -> _PushTables:
+def pull_tables(layout: RemapLayout, rank: int, inverse: bool, device,
+                stager: TableStager | None = None) -> _PushTables:
     """Per-source rows for zp_remap_pull (forward: attention -> linear)."""
     w = layout.world
     m = layout.matrix
@@ -543,8 +596,11 @@ def pull_tables(layout: RemapLayout, rank: int, inverse: bool, device) -> _PushT
         dst0 = layout.send_offsets(rank)
         readers = [int(m[s, rank] > 0) for s in range(w)]
     host = torch.tensor([src0, dst0, count, readers], dtype=torch.int32)
-    return _PushTables(host.pin_memory().to(device, non_blocking=True), max(count) if count else 0,
-                       np.ascontiguousarray(host.numpy()))
+    if stager is not None:
+        dev = stager.upload(host.numpy().reshape(-1)).view(4, w)
+    else:
+        dev = host.pin_memory().to(device, non_blocking=True)
+    return _PushTables(dev, max(count) if count else 0, np.ascontiguousarray(host.numpy()))
 
 
 def remap_pull(layout: RemapLayout, src: PeerBuffer, out: torch.Tensor, ctx: RankContext,
@@ -610,7 +666,15 @@ class ZeppelinLayer:
         self.plan = build_plan(batch, self.cluster)
         self.schedule = build_schedule(self.plan)
         self.program = build_rank_program(self.plan, self.schedule, self.ctx.rank, self.n_heads)
-        self.device_program = DeviceProgram(self.program, self.ctx.device)
+        if not hasattr(self, "_stager"):
+            self._stager = TableStager(self.ctx.device)
+            self._remap_stager = TableStager(self.ctx.device)
+        self.device_program = DeviceProgram(self.program, self.ctx.device, self._stager)
+        self._pull = None
+        if self.ctx.world > 1 and self.remap_method == "pull":
+            lay, r, dev = self.program.remap, self.ctx.rank, self.ctx.device
+            self._pull = (pull_tables(lay, r, False, dev, self._remap_stager),
+                          pull_tables(lay, r, True, dev, self._remap_stager))
         return self.plan
 
     @property
@@ -674,8 +738,9 @@ class ZeppelinLayer:
             attention_forward(self.plan, self.schedule, q, k, v, ctx, self.program, self.device_program,
                               out=(o, lse))
             if self.remap_method == "pull":
-                remap_pull(self.layout, peer, act, ctx)
-                remap_pull(self.layout, peer, act, ctx, inverse=True)
+                fw, inv = self._pull or (None, None)
+                remap_pull(self.layout, peer, act, ctx, tables=fw)
+                remap_pull(self.layout, peer, act, ctx, inverse=True, tables=inv)
             else:
                 remap_push(self.layout, act[:rows], peer, ctx)
                 remap_push(self.layout, act[:self.layout.linear_rows[ctx.rank]], peer, ctx, inverse=True)
@@ -724,7 +789,7 @@ class ZeppelinLayer:
         attention_forward(self.plan, self.schedule, q, k, v, self.ctx, self.program, self.device_program,
                           out=(o, lse))
         if self.remap_method == "pull":
-            y = remap_pull(self.layout, self.peer, buf, self.ctx)
+            y = remap_pull(self.layout, self.peer, buf, self.ctx, tables=(self._pull or (None, None))[0])
         else:
             y = remap_push(self.layout, buf[:rows], self.peer, self.ctx)
         return o, lse, y[:self.layout.linear_rows[self.ctx.rank]]
@@ -737,7 +802,8 @@ class ZeppelinLayer:
         if y.data_ptr() != self.peer.buf.data_ptr():
             self.peer.buf[:y.shape[0]].copy_(y)
         if self.remap_method == "pull":
-            x = remap_pull(self.layout, self.peer, self.peer.buf, self.ctx, inverse=True)
+            x = remap_pull(self.layout, self.peer, self.peer.buf, self.ctx, inverse=True,
+                           tables=(self._pull or (None, None))[1])
         else:
             x = remap_push(self.layout, self.peer.buf[:self.layout.linear_rows[r]], self.peer, self.ctx,
                            inverse=True)
