@@ -112,7 +112,10 @@ class TableStager:
             cap = max(n, 1 << 16)
             slot = {"pin": torch.empty(cap, dtype=torch.int32).pin_memory(),
                     "dev": torch.empty(cap, dtype=torch.int32, device=self.device),
-                    "copied": None, "consumed": None}
+                    "copied": None, "consumed": torch.cuda.Event()}
+            # the new block comes from the compute stream's pool: kernels still
+            # in flight there may have used this memory — the copy waits for them
+            slot["consumed"].record(cs)
             self.slots[self.turn - 1] = slot
         if slot["copied"] is not None:
             slot["copied"].synchronize()  # the previous copy out of this pinned slot is done
@@ -707,6 +710,8 @@ class ZeppelinLayer:
         slot = self._slots[self._turn]
         self._turn ^= 1
         key = (rows, hq, k_h.shape[1], d)
+        cs = torch.cuda.current_stream(dev)
+        fresh = None
         if slot.get("key") != key:
             slot["q"] = torch.empty(rows, hq, d, dtype=torch.bfloat16, device=dev)
             slot["k"] = torch.empty(rows, k_h.shape[1], d, dtype=torch.bfloat16, device=dev)
@@ -715,9 +720,14 @@ class ZeppelinLayer:
                 slot["own_act"] = torch.empty(max(rows, max(self.layout.linear_rows), 1), hq * d,
                                               dtype=torch.bfloat16, device=dev)
             slot["key"] = key
-        cs = torch.cuda.current_stream(dev)
+            # fresh blocks come from the compute stream's pool; the copy stream
+            # must not write them before earlier kernels there are done
+            fresh = torch.cuda.Event()
+            fresh.record(cs)
         ready = torch.cuda.Event()
         with torch.cuda.stream(self._h2d):
+            if fresh is not None:
+                self._h2d.wait_event(fresh)
             if slot["used"]:
                 self._h2d.wait_event(slot["free"])  # step i-2 no longer reads this slot's inputs
             slot["q"].copy_(q_h, non_blocking=True)
