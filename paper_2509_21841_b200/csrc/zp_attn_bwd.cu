@@ -20,14 +20,16 @@
 // for every tcgen05.mma:
 //   S^T  = K  Q^T    (M=128 keys, N=64 queries, K=128 dims)   -> TMEM
 //   dP^T = V  dO^T   (same shape)                              -> TMEM
-//   dV  += P^T dO    (M=128 keys, N=128 dims, K=64 queries)   -> TMEM, whole item
-//   dK  += dS^T Q    (same shape)                              -> TMEM, whole item
+//   dV  += P^T dO    (M=128 keys, N=128 dims, K=64 queries; A in TMEM) -> TMEM
+//   dK  += dS^T Q    (same shape, A in TMEM)                            -> TMEM
 //   dQ^T = K^T dS^T  (M=128 dims, N=64 queries, K=128 keys)    -> TMEM, then
 //                     fp32 reductions into the dQ accumulator
 // TMEM (512 columns): S^T/dQ^T buffers [0,128) (2 x 64), dP^T [128,256)
-// (2 x 64), dV [256,384), dK [384,512).  P^T and dS^T are written by the
-// softmax warps to shared memory in the SWIZZLE_128B K-major layout, which is
-// the A operand of dV/dK and (read MN-major) the B operand of dQ^T.
+// (2 x 64), dV [256,384), dK [384,512).  The softmax warps write P^T (bf16x2)
+// over the S^T columns they have read and dS^T over the dP^T columns: they are
+// the TMEM A operands of dV += P^T dO and dK += dS^T Q (no shared-memory A
+// traffic).  dS^T also goes to shared memory (SWIZZLE_128B, K-major rows of
+// 64 queries) as the MN-major B operand of dQ^T.
 //
 // Roles (384 threads): warp 0 TMA producer (K, V once; Q, dO per step,
 // double-buffered), warp 1 TMEM allocator + MMA issuer, warps 4-7 P/dS
@@ -53,9 +55,10 @@ constexpr uint32_t kSmemK = 0;
 constexpr uint32_t kSmemV = kSmemK + kKVTile;
 constexpr uint32_t kSmemQ = kSmemV + kKVTile;     // 2 buffers
 constexpr uint32_t kSmemDO = kSmemQ + 2 * kQTile; // 2 buffers
-constexpr uint32_t kSmemPT = kSmemDO + 2 * kQTile;
-constexpr uint32_t kSmemDST = kSmemPT + 2 * kPTile;
-constexpr uint32_t kSmemScr = kSmemDST + 2 * kPTile;  // per softmax warp: lse2[64], delta[64]
+constexpr uint32_t kSmemDST = kSmemDO + 2 * kQTile;
+constexpr uint32_t kSmemDQ = kSmemDST + 2 * kPTile;   // dQ staging: 4 boxes [64 queries][32 dims] fp32
+constexpr uint32_t kDQBox = kBQ * 32 * 4;             // 8 KB
+constexpr uint32_t kSmemScr = kSmemDQ + 4 * kDQBox;   // per softmax warp: lse2[64], delta[64]
 constexpr uint32_t kSmemBar = kSmemScr + 4 * 512;
 constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;
 
@@ -116,11 +119,40 @@ struct StepCursor {
   __device__ __forceinline__ int valid() const { return min(kBQ, g.len - b * kBQ); }
 };
 
+#ifdef ZP_TRACE
+__device__ unsigned long long g_zp_btrace[4096];
+#define ZP_BSTAMP(slot)                                                  \
+  do {                                                                   \
+    if (blockIdx.x == 0 && (slot) >= 0 && (slot) < 4096) {               \
+      unsigned long long c_;                                             \
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_)::"memory");        \
+      g_zp_btrace[slot] = c_;                                            \
+    }                                                                    \
+  } while (0)
+#else
+#define ZP_BSTAMP(slot) \
+  do {                  \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-__device__ __forceinline__ void red_add_f32(float* p, float v) {
-  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+// TMA reduce-add of a shared-memory tile into global fp32 (atomic per element in L2).
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* m, uint32_t src, int x, int y) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(x), "r"(y), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void st_shared_f32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
@@ -136,7 +168,7 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int cc) {
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                    const BwdArgs args) {
+                    const __grid_constant__ CUtensorMap tm_dq, const BwdArgs args) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t sbase = (raw + 1023u) & ~1023u;
@@ -213,8 +245,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t do_kmaj = umma_desc_sw128(sbase + kSmemDO, 16, 1024);
       const uint64_t q_mn = umma_desc_sw128(sbase + kSmemQ, kQBox, 1024);
       const uint64_t do_mn = umma_desc_sw128(sbase + kSmemDO, kQBox, 1024);
-      const uint64_t pt_k = umma_desc_sw128(sbase + kSmemPT, 16, 1024);
-      const uint64_t dst_k = umma_desc_sw128(sbase + kSmemDST, 16, 1024);
       const uint64_t dst_mn = umma_desc_sw128(sbase + kSmemDST, kPTile, 1024);
       constexpr uint64_t q_step = kQTile >> 4, p_step = kPTile >> 4;
 
@@ -250,13 +280,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int buf = n & 1;
         mbar_wait(bar(B_PDS_FULL + buf), (n >> 1) & 1);
         tc_fence_after();
+        if (lane == 0 && n < 256) ZP_BSTAMP(2048 + n * 4 + 0);
 #pragma unroll 1
         for (int kk = 0; kk < kBQ / 16; ++kk) {
           const uint32_t acc = (n > 0 || kk > 0) ? 1u : 0u;
-          mma_ss_w(tDV, pt_k + p_step * buf + ((kk * 32) >> 4), do_mn + q_step * buf + ((kk * 2048) >> 4),
-                 idesc_kv, acc);
-          mma_ss_w(tDK, dst_k + p_step * buf + ((kk * 32) >> 4), q_mn + q_step * buf + ((kk * 2048) >> 4),
-                 idesc_kv, acc);
+          // A = P^T / dS^T straight from TMEM (bf16x2, 8 columns per 16 queries)
+          mma_ts_w(tDV, tS0 + 64 * buf + kk * 8, do_mn + q_step * buf + ((kk * 2048) >> 4), idesc_kv, acc);
+          mma_ts_w(tDK, tDP0 + 64 * buf + kk * 8, q_mn + q_step * buf + ((kk * 2048) >> 4), idesc_kv, acc);
         }
         tc_commit_w(bar(B_QDO_EMPTY + buf));
 #pragma unroll 1
@@ -265,6 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                  kk > 0 ? 1u : 0u);
         tc_commit_w(bar(B_DQ_FULL + buf));
         tc_commit_w(bar(B_PDS_EMPTY + buf));
+        if (lane == 0 && n < 256) ZP_BSTAMP(2048 + n * 4 + 1);
       }
       tc_commit_w(bar(B_DKV));
     }
@@ -295,11 +326,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         scr[64 + j] = ok ? args.delta[ix] : 0.f;
       }
       __syncwarp();
+      const int tr = (lane == 0 && quad == 0 && n < 256) ? n * 4 : -1;
+      ZP_BSTAMP(tr);
       mbar_wait(bar(B_SDP_FULL + buf), (n >> 1) & 1);
       tc_fence_after();
+      ZP_BSTAMP(tr < 0 ? -1 : tr + 1);
       if (n >= 2) mbar_wait(bar(B_PDS_EMPTY + buf), ((n >> 1) - 1) & 1);
+      ZP_BSTAMP(tr < 0 ? -1 : tr + 2);
       const bool full = kval && it.kv_len == kBK && qpos0 >= it.kv_pos0 + kBK - 1;
-      const uint32_t pt_row = sbase + kSmemPT + buf * kPTile;
       const uint32_t dst_row = sbase + kSmemDST + buf * kPTile;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -333,17 +367,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           dk[j / 2] = pack_bf16(ds[0], ds[1]);
           dk[j / 2 + 1] = pack_bf16(ds[2], ds[3]);
         }
+        // P^T / dS^T (bf16x2) over the S^T / dP^T columns this chunk has already
+        // read (chunk c covers columns [32c, 32c+32) and writes [16c, 16c+16));
+        // they are the TMEM A operands of dV += P^T dO and dK += dS^T Q.
+        tmem_st16(tS0 + lane_bits + 64 * buf + 16 * c, pk);
+        tmem_st16(tDP0 + lane_bits + 64 * buf + 16 * c, dk);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint32_t off = sw128_off(k, 4 * c + i);
-          st_shared_v4(pt_row + off, pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-          st_shared_v4(dst_row + off, dk[4 * i], dk[4 * i + 1], dk[4 * i + 2], dk[4 * i + 3]);
-        }
+        for (int i = 0; i < 4; ++i)
+          st_shared_v4(dst_row + sw128_off(k, 4 * c + i), dk[4 * i], dk[4 * i + 1], dk[4 * i + 2], dk[4 * i + 3]);
       }
       fence_proxy_async_smem();  // generic-proxy smem writes -> tcgen05.mma operands
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar(B_PDS_FULL + buf));
+      ZP_BSTAMP(tr < 0 ? -1 : tr + 3);
     }
     // ---------------- dK / dV of this key tile (fp32, accumulated if asked)
     mbar_wait(bar(B_DKV), 0);
@@ -379,18 +417,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 8) {
-    // ---------------- dQ reduction (thread == head dim)
+    // ---------------- dQ reduction (thread == head dim): the dQ^T tile goes
+    // through a shared-memory staging tile ([64 queries][128 dims] as four
+    // 32-dim boxes) and leaves with four TMA reduce-adds (atomic in L2).
+    // Query rows past the segment end carry exact zeros (P = dS = 0 there).
     const int quad = warp & 3;
-    const int dcol = quad * 32 + lane;
     const uint32_t lane_bits = uint32_t(quad * 32) << 16;
-    const size_t qstride = size_t(args.hq) * kD;
+    const uint32_t stage = sbase + kSmemDQ + quad * kDQBox + lane * 4;
+    const bool issuer = warp == 8 && lane == 0;
     StepCursor cur(args.qsegs, it.qseg_begin, it.qseg_count, it.kv_pos0, args.group);
     for (int n = 0; cur.next(); ++n) {
       const int buf = n & 1;
       const int h = kvh * args.group + cur.hh;
-      const int qrow0 = cur.row(), qv = cur.valid();
       mbar_wait(bar(B_DQ_FULL + buf), (n >> 1) & 1);
       tc_fence_after();
+      if (lane == 0 && quad == 0 && n < 256) ZP_BSTAMP(1024 + n * 4);
       uint32_t r0[32], r1[32];
       tmem_ld32(tS0 + lane_bits + 64 * buf, r0);
       tmem_ld32(tS0 + lane_bits + 64 * buf + 32, r1);
@@ -398,14 +439,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar(B_DQ_EMPTY + buf));
-      float* dst = args.dq + (size_t(qrow0) * args.hq + h) * kD + dcol;
+      if (issuer) bulk_wait_read0();  // the previous reduce has read the staging tile
+      named_bar_sync(1, 128);
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < qv) red_add_f32(dst + j * qstride, __uint_as_float(r0[j]) * args.scale);
+      for (int j = 0; j < 32; ++j) st_shared_f32(stage + j * 128, __uint_as_float(r0[j]) * args.scale);
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (32 + j < qv) red_add_f32(dst + (32 + j) * qstride, __uint_as_float(r1[j]) * args.scale);
+      for (int j = 0; j < 32; ++j) st_shared_f32(stage + (32 + j) * 128, __uint_as_float(r1[j]) * args.scale);
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (issuer) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          tma_reduce_add_2d(&tm_dq, sbase + kSmemDQ + b * kDQBox, h * kD + 32 * b, cur.row());
+        bulk_commit();
+      }
+      if (lane == 0 && quad == 0 && n < 256) ZP_BSTAMP(1024 + n * 4 + 1);
     }
+    if (issuer) bulk_wait0();
   }
 
   tc_fence_before();
@@ -443,6 +493,13 @@ __global__ void bwd_delta_kernel(const __nv_bfloat16* __restrict__ o, const __nv
 // ------------------------------------------------------------------ host side
 #include "zp_host.h"
 
+#ifdef ZP_TRACE
+extern "C" ZP_API int zp_debug_btrace(unsigned long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, zp::bwd::g_zp_btrace, sizeof(unsigned long long) * (n < 4096 ? n : 4096)) ==
+                 cudaSuccess ? 0 : -1;
+}
+#endif
+
 extern "C" int zp_attn_bwd_prep(const void* o, const void* dout, int rows, int hq, int head_dim, float* delta,
                                 int delta_stride, void* stream) {
   using namespace zp::bwd;
@@ -476,7 +533,7 @@ extern "C" int zp_attn_bwd(const void* q, const void* k, const void* v, const vo
     return zp_fail(ZP_EINVAL, "zp_attn_bwd: null pointer");
   if (zp_check_device() != ZP_OK) return ZP_ENODEV;
 
-  CUtensorMap tq, tdo, tk, tv;
+  CUtensorMap tq, tdo, tk, tv, tdq;
   int rc;
   if ((rc = zp_make_tmap_2d_bf16(&tq, q, uint64_t(hq) * kD, uint64_t(q_rows), uint64_t(hq) * kD * 2, 64, kBQ)) !=
       ZP_OK)
@@ -489,6 +546,9 @@ extern "C" int zp_attn_bwd(const void* q, const void* k, const void* v, const vo
     return rc;
   if ((rc = zp_make_tmap_2d_bf16(&tv, v, uint64_t(hkv) * kD, uint64_t(kv_rows), uint64_t(kv_row_stride) * 2, 64,
                                  kBK)) != ZP_OK)
+    return rc;
+  if ((rc = zp_make_tmap_2d_f32(&tdq, dq, uint64_t(hq) * kD, uint64_t(q_rows), uint64_t(hq) * kD * 4, 32, kBQ)) !=
+      ZP_OK)
     return rc;
   static bool attr_done = false;
   if (!attr_done) {
@@ -511,7 +571,8 @@ extern "C" int zp_attn_bwd(const void* q, const void* k, const void* v, const vo
   a.group = hq / hkv;
   a.scale = softmax_scale;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
-  attn_bwd_kernel<<<n_items, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(tq, tdo, tk, tv, a);
+  attn_bwd_kernel<<<n_items, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(tq, tdo, tk, tv, tdq,
+                                                                                              a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return zp_fail_cuda(e, "zp_attn_bwd: launch");
   return ZP_OK;

@@ -76,6 +76,25 @@ int zp_make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t cols, uint
   return ZP_OK;
 }
 
+int zp_make_tmap_2d_f32(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
+                        uint64_t row_pitch_bytes, uint32_t box_cols, uint32_t box_rows) {
+  if ((reinterpret_cast<uintptr_t>(base) & 15u) || (row_pitch_bytes & 15u))
+    return zp_fail(ZP_EINVAL, "tensor map: base and row pitch must be 16-byte aligned");
+  if (zp_check_device() != ZP_OK) return ZP_ENODEV;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {row_pitch_bytes};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    std::snprintf(g_err, sizeof(g_err), "cuTensorMapEncodeTiled (f32) failed (CUresult %d)", int(r));
+    return ZP_ETMA;
+  }
+  return ZP_OK;
+}
+
 extern "C" const char* zp_last_error(void) { return g_err; }
 
 extern "C" int zp_version(void) { return 1; }

@@ -13,3 +13,7 @@ int zp_check_device();
 // row pitch in bytes, box (box_cols x box_rows), SWIZZLE_128B, OOB -> zero.
 int zp_make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
                          uint64_t row_pitch_bytes, uint32_t box_cols, uint32_t box_rows);
+// 2-D fp32 tensor map without swizzle (row-major staging tiles, e.g. the
+// TMA reduce-add of the backward's dQ).
+int zp_make_tmap_2d_f32(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
+                        uint64_t row_pitch_bytes, uint32_t box_cols, uint32_t box_rows);
