@@ -152,7 +152,14 @@ struct TileCursor {
   __device__ __forceinline__ int valid() const { return min(kBN, g.len - ti * kBN); }
 };
 
-constexpr float kRescaleLog2 = 8.0f;  // lazy-rescale threshold (log2 units)
+#ifndef ZP_RESCALE_LOG2
+#define ZP_RESCALE_LOG2 8.0f
+#endif
+constexpr float kRescaleLog2 = ZP_RESCALE_LOG2;  // lazy-rescale threshold (log2 units)
+#ifndef ZP_SPEC_EXP
+#define ZP_SPEC_EXP 1
+#endif
+constexpr bool kSpecExp = ZP_SPEC_EXP != 0;  // speculative exps with the running max
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
@@ -587,19 +594,74 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < 128; ++c)
             if (c > lim) s[c] = -INFINITY;
         }
-        // row max with 3-input max (FMNMX3), four independent chains
-        float mx0 = fmax3(s[0], s[1], s[2]), mx1 = fmax3(s[3], s[4], s[5]);
-        float mx2 = fmax3(s[6], s[7], s[8]), mx3 = fmax3(s[9], s[10], s[11]);
+        float mx;  // row max in log2 units
+        bool have_mx = false;
+        if (kSpecExp && __all_sync(0xffffffffu, m > -INFINITY)) {
+          // Speculative path: with a finite reference max, the first half's
+          // exponentials start right away with it while the row max is folded
+          // in alongside (ALU next to MUFU); only if some row exceeds the
+          // reference by more than the lazy threshold is the work redone.
+          const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m, -m);
+          float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+          uint32_t pa0[16], pa1[16];
+          float c0 = -INFINITY, c1 = -INFINITY, c2 = -INFINITY, c3 = -INFINITY;
 #pragma unroll
-        for (int c = 12; c < 124; c += 8) {
-          mx0 = fmax3(mx0, s[c], s[c + 1]);
-          mx1 = fmax3(mx1, s[c + 2], s[c + 3]);
-          mx2 = fmax3(mx2, s[c + 4], s[c + 5]);
-          mx3 = fmax3(mx3, s[c + 6], s[c + 7]);
+          for (int v = 0; v < 32; ++v) {
+            const float2 x = __ffma2_rn(make_float2(s[2 * v], s[2 * v + 1]), sl2x2, negm);
+            float2 p;
+            p.x = ex2(x.x);
+            p.y = ex2(x.y);
+            if (v & 1) a1 = __fadd2_rn(a1, p); else a0 = __fadd2_rn(a0, p);
+            if (v < 16) pa0[v] = pack_bf16(p.x, p.y); else pa1[v - 16] = pack_bf16(p.x, p.y);
+            if (v & 1) {
+              c0 = fmax3(c0, s[2 * v], s[2 * v + 1]);
+              c1 = fmax3(c1, s[64 + 2 * v], s[64 + 2 * v + 1]);
+            } else {
+              c2 = fmax3(c2, s[2 * v], s[2 * v + 1]);
+              c3 = fmax3(c3, s[64 + 2 * v], s[64 + 2 * v + 1]);
+            }
+          }
+          mx = fmax3(c0, c1, fmaxf(c2, c3)) * sl2;
+          have_mx = true;
+          if (!__any_sync(0xffffffffu, mx > m + kRescaleLog2)) {
+            tmem_st16(tP, pa0);
+            tmem_st16(tP + 16, pa1);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if constexpr (kPair) mbar_arrive_remote(pfull);
+              else mbar_arrive(pfull);
+            }
+            if (masked) exp_half<1, false>(s, sl2x2, negm, tP, a0, a1);
+            else exp_half<1, true>(s, sl2x2, negm, tP, a0, a1);
+            const float2 acc = __fadd2_rn(a0, a1);
+            l += acc.x + acc.y;
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if constexpr (kPair) mbar_arrive_remote(pfull + 8);
+              else mbar_arrive(pfull + 8);
+            }
+            continue;
+          }
         }
-        mx0 = fmax3(mx0, s[124], s[125]);
-        mx1 = fmax3(mx1, s[126], s[127]);
-        const float mx = fmax3(mx0, mx1, fmaxf(mx2, mx3)) * sl2;
+        if (!have_mx) {
+          // row max with 3-input max (FMNMX3), four independent chains
+          float mx0 = fmax3(s[0], s[1], s[2]), mx1 = fmax3(s[3], s[4], s[5]);
+          float mx2 = fmax3(s[6], s[7], s[8]), mx3 = fmax3(s[9], s[10], s[11]);
+#pragma unroll
+          for (int c = 12; c < 124; c += 8) {
+            mx0 = fmax3(mx0, s[c], s[c + 1]);
+            mx1 = fmax3(mx1, s[c + 2], s[c + 3]);
+            mx2 = fmax3(mx2, s[c + 4], s[c + 5]);
+            mx3 = fmax3(mx3, s[c + 6], s[c + 7]);
+          }
+          mx0 = fmax3(mx0, s[124], s[125]);
+          mx1 = fmax3(mx1, s[126], s[127]);
+          mx = fmax3(mx0, mx1, fmaxf(mx2, mx3)) * sl2;
+        }
 #ifdef ZP_TRACE
         asm volatile("" ::"f"(mx));
         ZP_STAMP(tr < 0 ? -1 : tr + 2);
