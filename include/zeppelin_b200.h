@@ -85,7 +85,10 @@ typedef struct zp_kv_seg {
  * touched by items carrying ZP_ITEM_*_STATE.  Items must be device-resident.
  * workspace: >= ZP_ATTN_WORKSPACE_BYTES of device memory owned by the caller
  * (the persistent CTAs' work counter; zeroed by the call on `stream`).  Items
- * are claimed in list order, so pass them longest-first. */
+ * are claimed in list order, so pass them longest-first.
+ * When (hq/hkv) % 4 == 0 the kernel runs CTA pairs (cta_group::2): items 2p
+ * and 2p+1 must then describe the same query tile for head pairs 2g and 2g+1
+ * (the order worklist.build_worklist emits); a violation traps the kernel. */
 #define ZP_ATTN_WORKSPACE_BYTES 16
 ZP_API int zp_attn_fwd(const void* q, const void* k, const void* v, int q_rows, int kv_rows,
                 int kv_row_stride, int hq, int hkv, int head_dim, void* o, float* lse,

@@ -390,6 +390,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (idx >= n_units) break;
         const zp_attn_item it = args.items[kPair ? 2 * idx + int(cta) : idx];
+        if constexpr (kPair) {
+          // contract: items 2p / 2p+1 are the same tile for head pairs 2g / 2g+1
+          const zp_attn_item o = args.items[2 * idx + 1 - int(cta)];
+          if (o.q_row0 != it.q_row0 || o.q_pos0 != it.q_pos0 || o.q_len != it.q_len ||
+              o.seg_begin != it.seg_begin || o.seg_count != it.seg_count || o.state_row0 != it.state_row0 ||
+              o.flags != it.flags || it.head_pair != (o.head_pair ^ 1) || (it.head_pair & 1) != int(cta))
+            __trap();
+        }
         if (count_tiles(args.segs, it) == 0) continue;
         const int kvh = (2 * it.head_pair) / args.group;
         if (qn > 0) mbar_wait(bar(B_QEMPTY), (qn - 1) & 1);

@@ -114,3 +114,29 @@ def test_host_fed_pipeline_matches_device_path():
         o, _ = layer.attention(hq_[i].cuda(), hk_[i].cuda(), hv_[i].cuda())
         torch.cuda.synchronize()
         assert torch.equal(outs[i], o.cpu()), f"step {i} differs"
+
+
+def test_pair_contract_violation_fails_loudly():
+    """With GQA group 4 the kernel runs CTA pairs; an item list whose pairs do
+    not match (here: head pairs swapped) must abort the launch, not return
+    wrong numbers.  Run in a child process (a trapped kernel poisons the CUDA
+    context)."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, torch
+sys.path.insert(0, ".")
+from paper_2509_21841_b200 import ops
+from paper_2509_21841_b200.worklist import build_worklist
+q = torch.randn(256, 32, 128, device="cuda", dtype=torch.bfloat16)
+k = torch.randn(256, 8, 128, device="cuda", dtype=torch.bfloat16)
+wl = build_worklist(ops.local_fragments([256]), 16)
+wl.items["head_pair"][0], wl.items["head_pair"][1] = 1, 0
+items, segs = ops.upload_worklist(wl, q.device)
+o = torch.empty_like(q); lse = torch.empty(32, 256, device="cuda")
+ops.attn_fwd(q, k, k, items, wl.n_items, segs, o, lse)
+torch.cuda.synchronize()
+print("NO ERROR")
+'''
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert "NO ERROR" not in r.stdout and r.returncode != 0, r.stdout + r.stderr
