@@ -326,54 +326,93 @@ class BwdDeviceProgram:
 
 def _run_ring_backward(ctx: RankContext, rp, dev_pack, dev_rounds, dev_unpack, q, k, v, dout, lse, delta,
                        dq, dk, dv, scale):
-    """Ring backward: round r computes dQ (accumulated in place) and the
-    contribution of this rank's queries to dK/dV of the KV set it holds; the
-    partial dK/dV travel with the KV set to position i+1, and after the last
-    round one more hop returns every set's gradient to its owner."""
+    """Ring backward.  Round r computes dQ (accumulated in place) and this
+    position's contribution Z_r to dK/dV of the KV set it holds, into fresh
+    buffers.  On the comm stream, while round r+1 computes, the partial sum A_r
+    received from position i-1 is added (T_r = A_r + Z_r) and forwarded to
+    i+1, and the KV set for round r+2 moves one hop; after the last round the
+    same exchange returns every set's total gradient to its owner (the
+    reference charges g sends per ring, README.md:119-124).  The compute
+    stream waits only for KV sets, never for gradients."""
     hkv, d = k.shape[1], k.shape[2]
     g = rp.group_size
     rows = max(rp.held_rows)
+    cs, xs = torch.cuda.current_stream(), ctx.comm_stream
     kv = [ctx.workspace(f"ringkv{j}", (rows, 2, hkv, d), torch.bfloat16) for j in (0, 1)]
-    gk = [ctx.workspace(f"ringdk{j}", (rows, hkv, d), torch.float32) for j in (0, 1)]
-    gv = [ctx.workspace(f"ringdv{j}", (rows, hkv, d), torch.float32) for j in (0, 1)]
+    # own contribution (z) and received partial (a) for dK and dV, fp32, double-buffered
+    zk = [ctx.workspace(f"ring_zk{j}", (rows, hkv, d), torch.float32) for j in (0, 1)]
+    zv = [ctx.workspace(f"ring_zv{j}", (rows, hkv, d), torch.float32) for j in (0, 1)]
+    ak = [ctx.workspace(f"ring_ak{j}", (rows, hkv, d), torch.float32) for j in (0, 1)]
+    av = [ctx.workspace(f"ring_av{j}", (rows, hkv, d), torch.float32) for j in (0, 1)]
     n_pack = rp.pack_ranges.shape[0]
     max_pack = int(rp.pack_ranges[:, 2].max()) if n_pack else 0
     ops.copy_rows(kv[0][:, 0], k, dev_pack, n_pack, max_pack)
     ops.copy_rows(kv[0][:, 1], v, dev_pack, n_pack, max_pack)
-    gk[0].zero_()
-    gv[0].zero_()
+    start = torch.cuda.Event()
+    start.record(cs)
+    xs.wait_event(start)  # buffers (fresh from the compute stream's pool) and the packed set are ready
+    kv_ready = start
+    z_free = [None, None]
     for r in range(g):
         cur, nxt = r % 2, (r + 1) % 2
+        # -- KV set for round r+1 moves one hop (overlaps this round's compute)
+        next_kv = None
+        if r < g - 1:
+            with torch.cuda.stream(xs), ctx.span("intra-comm", "kv.send",
+                                                  {"ring": rp.ring_index, "round": r, "tokens": rp.send_rows(r),
+                                                   "dst": rp.next_rank}, xs):
+                p2p = ring_p2p_ops(rp, r, kv[cur], kv[nxt], ctx.group)
+                if p2p:
+                    for req in dist.batch_isend_irecv(p2p):
+                        req.wait()
+            next_kv = torch.cuda.Event()
+            next_kv.record(xs)
+        # -- this round's gradients into fresh buffers
         n_kv = rp.rounds[r].kv_rows
+        if r > 0:
+            cs.wait_event(kv_ready)
+        if z_free[cur] is not None:
+            cs.wait_event(z_free[cur])  # what these buffers held two rounds ago has been forwarded
+        zk[cur][:n_kv].zero_()
+        zv[cur][:n_kv].zero_()
         work = dev_rounds[r]
         with ctx.span("compute", "intra_node.attn_bwd",
                       {"ring": rp.ring_index, "round": r, "pairs": rp.rounds[r].work.pairs_per_head}):
             if work.n:
-                ops.attn_bwd(q, kv[cur][:n_kv, 0], kv[cur][:n_kv, 1], dout, lse, delta, dq, gk[cur][:n_kv],
-                             gv[cur][:n_kv], work.items, work.n, work.segs, softmax_scale=scale)
-        # forward the KV set (not after the last round) and its gradient (always)
+                ops.attn_bwd(q, kv[cur][:n_kv, 0], kv[cur][:n_kv, 1], dout, lse, delta, dq, zk[cur][:n_kv],
+                             zv[cur][:n_kv], work.items, work.n, work.segs, softmax_scale=scale)
+        done = torch.cuda.Event()
+        done.record(cs)
+        # -- add the partial received for this set and forward it (comm stream)
         n_send, n_recv = rp.send_rows(r), rp.recv_rows(r)
-        p2p = []
-        with ctx.span("intra-comm", "dkv.send", {"ring": rp.ring_index, "round": r, "tokens": n_send,
-                                                  "dst": rp.next_rank}):
+        with torch.cuda.stream(xs), ctx.span("intra-comm", "dkv.send",
+                                              {"ring": rp.ring_index, "round": r, "tokens": n_send,
+                                               "dst": rp.next_rank}, xs):
+            xs.wait_event(done)
+            if r > 0 and n_send:
+                zk[cur][:n_send].add_(ak[cur][:n_send])
+                zv[cur][:n_send].add_(av[cur][:n_send])
+            p2p = []
             if n_send:
-                if r < g - 1:
-                    p2p.append(dist.P2POp(dist.isend, kv[cur][:n_send], rp.next_rank, ctx.group))
-                p2p += [dist.P2POp(dist.isend, gk[cur][:n_send], rp.next_rank, ctx.group),
-                        dist.P2POp(dist.isend, gv[cur][:n_send], rp.next_rank, ctx.group)]
+                p2p += [dist.P2POp(dist.isend, zk[cur][:n_send], rp.next_rank, ctx.group),
+                        dist.P2POp(dist.isend, zv[cur][:n_send], rp.next_rank, ctx.group)]
             if n_recv:
-                if r < g - 1:
-                    p2p.append(dist.P2POp(dist.irecv, kv[nxt][:n_recv], rp.prev_rank, ctx.group))
-                p2p += [dist.P2POp(dist.irecv, gk[nxt][:n_recv], rp.prev_rank, ctx.group),
-                        dist.P2POp(dist.irecv, gv[nxt][:n_recv], rp.prev_rank, ctx.group)]
+                p2p += [dist.P2POp(dist.irecv, ak[nxt][:n_recv], rp.prev_rank, ctx.group),
+                        dist.P2POp(dist.irecv, av[nxt][:n_recv], rp.prev_rank, ctx.group)]
             if p2p:
                 for req in dist.batch_isend_irecv(p2p):
                     req.wait()
-    own = g % 2  # buffer holding this rank's own set after the return hop
+        ev = torch.cuda.Event()
+        ev.record(xs)
+        z_free[cur] = ev
+        if next_kv is not None:
+            kv_ready = next_kv
+    cs.wait_stream(xs)
+    own = g % 2  # the return hop delivered this rank's own set total into a*[own]
     n_up = dev_unpack.numel() // 3
     if n_up:
-        ops.copy_rows(dk, gk[own], dev_unpack, n_up, max_pack)
-        ops.copy_rows(dv, gv[own], dev_unpack, n_up, max_pack)
+        ops.copy_rows(dk, ak[own], dev_unpack, n_up, max_pack)
+        ops.copy_rows(dv, av[own], dev_unpack, n_up, max_pack)
 
 
 def attention_backward(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
