@@ -39,14 +39,22 @@ def make_qkv(t, hq=32, hkv=8, seed=0):
     return q, k, v
 
 
-@pytest.mark.parametrize("seqlens", [[128], [1], [77], [300, 5, 129, 1000], [2048, 17, 640]])
-def test_varlen_local_matches_fp32(seqlens):
+@pytest.mark.parametrize("seqlens,qscale", [([128], 1.0), ([1], 1.0), ([77], 1.0), ([300, 5, 129, 1000], 1.0),
+                                            ([2048, 17, 640], 1.0), ([0, 64, 0, 129, 0], 1.0), ([8192], 1.0),
+                                            ([3000, 700], 6.0), ([1500], 0.05)])
+def test_varlen_local_matches_fp32(seqlens, qscale):
+    """Ragged / empty / long sequences; qscale 6 makes the running max move by
+    more than the lazy threshold many times (rescale and speculative-exp
+    fallback paths), 0.05 makes the softmax nearly flat."""
     t = sum(seqlens)
     q, k, v = make_qkv(t, seed=len(seqlens))
+    q = (q.float() * qscale).to(torch.bfloat16)
     o, lse = ops.varlen_attention(q, k, v, seqlens)
     torch.cuda.synchronize()
     r = 0
     for n in seqlens:
+        if n == 0:
+            continue
         pos = torch.arange(n, device="cuda")
         ro, rl = ref_attention(q[r:r + n], k[r:r + n], v[r:r + n], pos, pos)
         err = (o[r:r + n].float() - ro).abs().max().item()

@@ -21,6 +21,8 @@ def _ref_grads(q, k, v, dout, seqlens):
     outs = []
     r = 0
     for n in seqlens:
+        if n == 0:
+            continue
         qs = qf[r:r + n].transpose(0, 1)
         ks = kf[r:r + n].repeat_interleave(hq // hkv, dim=1).transpose(0, 1)
         vs = vf[r:r + n].repeat_interleave(hq // hkv, dim=1).transpose(0, 1)
@@ -37,17 +39,19 @@ def _check(name, got, ref):
     assert err <= TOL_REL * scale + TOL_ABS, f"{name}: max err {err:.3e} vs max |ref| {scale:.3e}"
 
 
-@pytest.mark.parametrize("seqlens,hq,hkv", [
-    ([1000], 32, 8),
-    ([300, 17, 129, 64, 1, 200], 32, 8),
-    ([2048, 511], 16, 8),
-    ([777], 4, 2),
+@pytest.mark.parametrize("seqlens,hq,hkv,qscale", [
+    ([1000], 32, 8, 1.0),
+    ([300, 17, 129, 64, 1, 200], 32, 8, 1.0),
+    ([2048, 511], 16, 8, 1.0),
+    ([777], 4, 2, 1.0),
+    ([0, 200, 0, 65], 32, 8, 1.0),
+    ([1500], 32, 8, 4.0),
 ])
-def test_local_backward_matches_fp32_autograd(seqlens, hq, hkv):
+def test_local_backward_matches_fp32_autograd(seqlens, hq, hkv, qscale):
     from paper_2509_21841_b200 import ops
     t = sum(seqlens)
     g = torch.Generator().manual_seed(7)
-    q = torch.randn(t, hq, 128, generator=g).to(torch.bfloat16).cuda()
+    q = (torch.randn(t, hq, 128, generator=g) * qscale).to(torch.bfloat16).cuda()
     k = torch.randn(t, hkv, 128, generator=g).to(torch.bfloat16).cuda()
     v = torch.randn(t, hkv, 128, generator=g).to(torch.bfloat16).cuda()
     dout = torch.randn(t, hq, 128, generator=g).to(torch.bfloat16).cuda()
