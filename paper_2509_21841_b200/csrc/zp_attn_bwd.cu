@@ -53,27 +53,28 @@ constexpr uint32_t kPTile = kBK * kBQ * 2;   // 16 KB (128 keys x 64 queries)
 
 constexpr uint32_t kSmemK = 0;
 constexpr uint32_t kSmemV = kSmemK + kKVTile;
-constexpr uint32_t kSmemQ = kSmemV + kKVTile;     // 2 buffers
-constexpr uint32_t kSmemDO = kSmemQ + 2 * kQTile; // 2 buffers
-constexpr uint32_t kSmemDST = kSmemDO + 2 * kQTile;
+constexpr uint32_t kSmemQ = kSmemV + kKVTile;     // kQStages buffers
+constexpr int kQStages = 3;                          // Q / dO ring depth (TMA latency > one step)
+constexpr uint32_t kSmemDO = kSmemQ + kQStages * kQTile;
+constexpr uint32_t kSmemDST = kSmemDO + kQStages * kQTile;
 constexpr uint32_t kSmemDQ = kSmemDST + 2 * kPTile;   // dQ staging: 4 boxes [64 queries][32 dims] fp32
 constexpr uint32_t kDQBox = kBQ * 32 * 4;             // 8 KB
-constexpr uint32_t kSmemScr = kSmemDQ + 4 * kDQBox;   // per softmax warp: lse2[64], delta[64]
-constexpr uint32_t kSmemBar = kSmemScr + 4 * 512;
+constexpr uint32_t kSmemBar = kSmemDQ + 4 * kDQBox;
 constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;
 
 enum : int {
   B_KV = 0,
-  B_QDO_FULL = 1,   // +buf
-  B_QDO_EMPTY = 3,  // +buf
-  B_SDP_FULL = 5,   // +buf
-  B_PDS_FULL = 7,   // +buf
-  B_PDS_EMPTY = 9,  // +buf
-  B_DQ_FULL = 11,   // +buf
-  B_DQ_EMPTY = 13,  // +buf
-  B_DKV = 15,
-  B_COUNT = 16
+  B_QDO_FULL = 1,   // +stage (3)
+  B_QDO_EMPTY = 4,  // +stage (3)
+  B_SDP_FULL = 7,   // +buf
+  B_PDS_FULL = 9,   // +buf
+  B_PDS_EMPTY = 11, // +buf
+  B_DQ_FULL = 13,   // +buf
+  B_DQ_EMPTY = 15,  // +buf
+  B_DKV = 17,
+  B_COUNT = 18
 };
+static_assert(kSmemBar + 256 + 1024 <= 232448, "smem budget");
 
 struct BwdArgs {
   const zp_bwd_item* items;
@@ -184,9 +185,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(bar(B_KV), 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kQStages; ++b) {
       mbar_init(bar(B_QDO_FULL + b), 1);
       mbar_init(bar(B_QDO_EMPTY + b), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
       mbar_init(bar(B_SDP_FULL + b), 1);
       mbar_init(bar(B_PDS_FULL + b), 4);
       mbar_init(bar(B_PDS_EMPTY + b), 1);
@@ -219,14 +222,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       StepCursor cur(args.qsegs, it.qseg_begin, it.qseg_count, it.kv_pos0, args.group);
       for (uint32_t n = 0; cur.next(); ++n) {
-        const int buf = n & 1;
-        if (n >= 2) mbar_wait(bar(B_QDO_EMPTY + buf), ((n >> 1) - 1) & 1);
-        mbar_expect_tx(bar(B_QDO_FULL + buf), 2 * kQTile);
+        const int qs = int(n % kQStages);
+        if (n >= uint32_t(kQStages)) mbar_wait(bar(B_QDO_EMPTY + qs), ((n / kQStages) - 1) & 1);
+        mbar_expect_tx(bar(B_QDO_FULL + qs), 2 * kQTile);
         const int h = kvh * args.group + cur.hh;
         for (int b = 0; b < 2; ++b) {
-          tma_load_2d(sbase + kSmemQ + buf * kQTile + b * kQBox, &tm_q, bar(B_QDO_FULL + buf), h * kD + b * 64,
+          tma_load_2d(sbase + kSmemQ + qs * kQTile + b * kQBox, &tm_q, bar(B_QDO_FULL + qs), h * kD + b * 64,
                       cur.row(), pol_q);
-          tma_load_2d(sbase + kSmemDO + buf * kQTile + b * kQBox, &tm_do, bar(B_QDO_FULL + buf),
+          tma_load_2d(sbase + kSmemDO + qs * kQTile + b * kQBox, &tm_do, bar(B_QDO_FULL + qs),
                       h * kD + b * 64, cur.row(), pol_q);
         }
       }
@@ -256,28 +259,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(bar(B_KV), 0);
       tc_fence_after();
       auto issue_sdp = [&](int m) {
-        const int buf = m & 1;
-        mbar_wait(bar(B_QDO_FULL + buf), (m >> 1) & 1);
+        const int buf = m & 1, qs = m % kQStages;
+        mbar_wait(bar(B_QDO_FULL + qs), (m / kQStages) & 1);
         if (m >= 2) mbar_wait(bar(B_DQ_EMPTY + buf), ((m >> 1) - 1) & 1);  // dQ^T(m-2) drained
         tc_fence_after();
 #pragma unroll 1
         for (int kk = 0; kk < kD / 16; ++kk) {
           const uint64_t ao = ((kk >> 2) * kKVBox + (kk & 3) * 32) >> 4;
           const uint64_t bo = ((kk >> 2) * kQBox + (kk & 3) * 32) >> 4;
-          mma_ss_w(tS0 + 64 * buf, k_kmaj + ao, q_kmaj + q_step * buf + bo, idesc_t, kk > 0 ? 1u : 0u);
+          mma_ss_w(tS0 + 64 * buf, k_kmaj + ao, q_kmaj + q_step * qs + bo, idesc_t, kk > 0 ? 1u : 0u);
         }
 #pragma unroll 1
         for (int kk = 0; kk < kD / 16; ++kk) {
           const uint64_t ao = ((kk >> 2) * kKVBox + (kk & 3) * 32) >> 4;
           const uint64_t bo = ((kk >> 2) * kQBox + (kk & 3) * 32) >> 4;
-          mma_ss_w(tDP0 + 64 * buf, v_kmaj + ao, do_kmaj + q_step * buf + bo, idesc_t, kk > 0 ? 1u : 0u);
+          mma_ss_w(tDP0 + 64 * buf, v_kmaj + ao, do_kmaj + q_step * qs + bo, idesc_t, kk > 0 ? 1u : 0u);
         }
         tc_commit_w(bar(B_SDP_FULL + buf));
       };
       if (n_steps > 0) issue_sdp(0);
       for (int n = 0; n < n_steps; ++n) {
         if (n + 1 < n_steps) issue_sdp(n + 1);
-        const int buf = n & 1;
+        const int buf = n & 1, qs = n % kQStages;
         mbar_wait(bar(B_PDS_FULL + buf), (n >> 1) & 1);
         tc_fence_after();
         if (lane == 0 && n < 256) ZP_BSTAMP(2048 + n * 4 + 0);
@@ -285,10 +288,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kk = 0; kk < kBQ / 16; ++kk) {
           const uint32_t acc = (n > 0 || kk > 0) ? 1u : 0u;
           // A = P^T / dS^T straight from TMEM (bf16x2, 8 columns per 16 queries)
-          mma_ts_w(tDV, tS0 + 64 * buf + kk * 8, do_mn + q_step * buf + ((kk * 2048) >> 4), idesc_kv, acc);
-          mma_ts_w(tDK, tDP0 + 64 * buf + kk * 8, q_mn + q_step * buf + ((kk * 2048) >> 4), idesc_kv, acc);
+          mma_ts_w(tDV, tS0 + 64 * buf + kk * 8, do_mn + q_step * qs + ((kk * 2048) >> 4), idesc_kv, acc);
+          mma_ts_w(tDK, tDP0 + 64 * buf + kk * 8, q_mn + q_step * qs + ((kk * 2048) >> 4), idesc_kv, acc);
         }
-        tc_commit_w(bar(B_QDO_EMPTY + buf));
+        tc_commit_w(bar(B_QDO_EMPTY + qs));
 #pragma unroll 1
         for (int kk = 0; kk < kBK / 16; ++kk)
           mma_ss_w(tS0 + 64 * buf, k_mn + ((kk * 2048) >> 4), dst_mn + p_step * buf + ((kk * 2048) >> 4), idesc_q,
@@ -304,28 +307,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quad = warp & 3;
     const int k = quad * 32 + lane;
     const uint32_t lane_bits = uint32_t(quad * 32) << 16;
-    float* scr = reinterpret_cast<float*>(sgen + kSmemScr + quad * 512);
-    const uint32_t scr_s = sbase + kSmemScr + quad * 512;
     const bool kval = k < it.kv_len;
     const int kpos = it.kv_pos0 + k;
     const float c1 = args.scale_log2;
     int n = 0;
     StepCursor cur(args.qsegs, it.qseg_begin, it.qseg_count, it.kv_pos0, args.group);
-    for (; cur.next(); ++n) {
-      const int buf = n & 1;
-      const int h = kvh * args.group + cur.hh;
-      const int qrow0 = cur.row(), qpos0 = cur.pos(), qv = cur.valid();
-      __syncwarp();
+    // LSE / Delta of the NEXT step are loaded one step ahead (the global-load
+    // latency used to sit on the critical path right after S^T landed)
+    StepCursor ahead = cur;
+    float nl[2], nd[2];
+    auto fetch = [&](const StepCursor& c) {
+      const int hh = kvh * args.group + c.hh;
 #pragma unroll
       for (int jj = 0; jj < 2; ++jj) {
         const int j = lane + 32 * jj;
-        const bool ok = j < qv;
-        const size_t ix = size_t(h) * args.lse_stride + qrow0 + j;
+        const bool ok = j < c.valid();
+        const size_t ix = size_t(hh) * args.lse_stride + c.row() + j;
         // invalid query rows: LSE = +inf makes P exactly 0
-        scr[j] = ok ? args.lse[ix] * 1.4426950408889634f : INFINITY;
-        scr[64 + j] = ok ? args.delta[ix] : 0.f;
+        nl[jj] = ok ? args.lse[ix] * 1.4426950408889634f : INFINITY;
+        nd[jj] = ok ? args.delta[ix] : 0.f;
       }
-      __syncwarp();
+    };
+    if (ahead.next()) fetch(ahead);
+    for (; cur.next(); ++n) {
+      const int buf = n & 1;
+      const int qpos0 = cur.pos(), qv = cur.valid();
+      // lane j holds LSE2 / Delta of queries j and 32 + j of this step
+      const float cl[2] = {nl[0], nl[1]}, cd[2] = {nd[0], nd[1]};
+      if (ahead.next()) fetch(ahead);
       const int tr = (lane == 0 && quad == 0 && n < 256) ? n * 4 : -1;
       ZP_BSTAMP(tr);
       mbar_wait(bar(B_SDP_FULL + buf), (n >> 1) & 1);
@@ -344,15 +353,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t pk[16], dk[16];
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
-          float4 l4, d4;
-          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                       : "=f"(l4.x), "=f"(l4.y), "=f"(l4.z), "=f"(l4.w)
-                       : "r"(scr_s + 4 * (32 * c + j)));
-          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                       : "=f"(d4.x), "=f"(d4.y), "=f"(d4.z), "=f"(d4.w)
-                       : "r"(scr_s + 256 + 4 * (32 * c + j)));
-          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
-          const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+          float lv[4], dv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            lv[u] = __shfl_sync(0xffffffffu, cl[c], j + u);
+            dv[u] = __shfl_sync(0xffffffffu, cd[c], j + u);
+          }
           float p[4], ds[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
