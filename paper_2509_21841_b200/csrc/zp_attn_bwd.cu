@@ -260,8 +260,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       auto issue_sdp = [&](int m) {
         const int buf = m & 1, qs = m % kQStages;
+        if (lane == 0 && m < 256) ZP_BSTAMP(3072 + m * 4 + 0);
         mbar_wait(bar(B_QDO_FULL + qs), (m / kQStages) & 1);
+        if (lane == 0 && m < 256) ZP_BSTAMP(3072 + m * 4 + 1);
         if (m >= 2) mbar_wait(bar(B_DQ_EMPTY + buf), ((m >> 1) - 1) & 1);  // dQ^T(m-2) drained
+        if (lane == 0 && m < 256) ZP_BSTAMP(3072 + m * 4 + 2);
         tc_fence_after();
 #pragma unroll 1
         for (int kk = 0; kk < kD / 16; ++kk) {
@@ -276,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_ss_w(tDP0 + 64 * buf, v_kmaj + ao, do_kmaj + q_step * qs + bo, idesc_t, kk > 0 ? 1u : 0u);
         }
         tc_commit_w(bar(B_SDP_FULL + buf));
+        if (lane == 0 && m < 256) ZP_BSTAMP(3072 + m * 4 + 3);
       };
       if (n_steps > 0) issue_sdp(0);
       for (int n = 0; n < n_steps; ++n) {
