@@ -59,13 +59,13 @@ constexpr int kMmaUnroll = ZP_MMA_UNROLL;
 // Diagnostic build only (-DZP_TRACE): SM clock stamps of CTA 0's softmax
 // stages and MMA issue points, read back with zp_debug_trace().
 #ifdef ZP_TRACE
-__device__ unsigned long long g_zp_trace[4096];
+__device__ unsigned long long g_zp_trace[8192];  // CTA 0 at [0, 4096), CTA 1 at [4096, 8192)
 #define ZP_STAMP(slot)                                                              \
   do {                                                                              \
-    if (blockIdx.x == 0 && (slot) >= 0 && (slot) < 4096) {                          \
+    if (blockIdx.x < 2 && (slot) >= 0 && (slot) < 4096) {                           \
       unsigned long long c_;                                                        \
       asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_)::"memory");                  \
-      g_zp_trace[slot] = c_;                                                        \
+      g_zp_trace[blockIdx.x * 4096 + (slot)] = c_;                                  \
     }                                                                               \
   } while (0)
 #else
@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) ZP_STAMP(4095);  // cluster-sync release: aligns the two CTAs' clocks
 
   // Next work unit for a consumer: wait for the slot, then release it to the
   // publishing producer (leader's ring in a pair).
@@ -458,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int h = 0; h < 2; ++h) {
           mbar_wait(bar(B_PFULL + 2 * t + h), (jg - 1) & 1);
           tc_fence_after();
-          if (lane == 0 && h == 0 && jg < 256) ZP_STAMP(2560 + int(jg) * 4 + 2 * t);
+          if (lane == 0 && jg < 255) ZP_STAMP(2560 + int(jg - 1) * 6 + 3 * t + h);
           issue_pv<kPair>(tO[t], tS[t] + 64, v_desc0 + v_step * pvs, idesc_pv, prev_acc, h);
         }
         commit<kPair>(bar(B_ODONE + t));
@@ -491,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int t = 0; t < 2; ++t) {
               issue_qk<kPair>(tS[t], q_desc0 + q_step * t, k_desc0 + k_step * kst, idesc_qk);
               commit<kPair>(bar(B_SFULL + t));
-              if (lane == 0 && jg < 256) ZP_STAMP(2560 + int(jg) * 4 + 2 * t + 1);
+              if (lane == 0 && jg < 255) ZP_STAMP(2560 + int(jg) * 6 + 3 * t + 2);
             }
           } else {
             for (int t = 0; t < 2; ++t) {
@@ -502,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               issue_qk<kPair>(tS[t], q_desc0 + q_step * t, k_desc0 + k_step * kst, idesc_qk);
               commit<kPair>(bar(B_SFULL + t));
-              if (lane == 0 && jg < 256) ZP_STAMP(2560 + int(jg) * 4 + 2 * t + 1);
+              if (lane == 0 && jg < 255) ZP_STAMP(2560 + int(jg) * 6 + 3 * t + 2);
             }
           }
           if (jg > 0) commit<kPair>(bar(B_VEMPTY + pvs));
@@ -641,6 +642,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               if constexpr (kPair) mbar_arrive_remote(pfull);
               else mbar_arrive(pfull);
             }
+            ZP_STAMP(tr < 0 ? -1 : tr + 2);
+            ZP_STAMP(tr < 0 ? -1 : tr + 3);
             if (masked) exp_half<1, false>(s, sl2x2, negm, tP, a0, a1);
             else exp_half<1, true>(s, sl2x2, negm, tP, a0, a1);
             const float2 acc = __fadd2_rn(a0, a1);
@@ -652,6 +655,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if constexpr (kPair) mbar_arrive_remote(pfull + 8);
               else mbar_arrive(pfull + 8);
             }
+            ZP_STAMP(tr < 0 ? -1 : tr + 4);
             continue;
           }
         }
@@ -1369,7 +1373,7 @@ int launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap&
 
 #ifdef ZP_TRACE
 extern "C" ZP_API int zp_debug_trace(unsigned long long* host, int n) {
-  return cudaMemcpyFromSymbol(host, zp::g_zp_trace, sizeof(unsigned long long) * (n < 4096 ? n : 4096)) ==
+  return cudaMemcpyFromSymbol(host, zp::g_zp_trace, sizeof(unsigned long long) * (n < 8192 ? n : 8192)) ==
                  cudaSuccess ? 0 : -1;
 }
 #endif

@@ -20,24 +20,53 @@ o = torch.empty_like(q); lse = torch.empty(32, t, device='cuda')
 for _ in range(2):
     ops.attn_fwd(q, k, v, items, wl.n_items, segs, o, lse)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * 4096)()
-assert _native.lib().zp_debug_trace(buf, 4096) == 0
-a = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
+buf = (ctypes.c_ulonglong * 8192)()
+assert _native.lib().zp_debug_trace(buf, 8192) == 0
+A = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
+med = lambda x: float(np.median(x))
+for cta in (0, 1):
+    a = A[cta * 4096:(cta + 1) * 4096]
+    sm = [a[tt * 1280: tt * 1280 + 1280].reshape(256, 5) for tt in range(2)]
+    n = int((sm[0][:, 0] > 0).sum())
+    if n == 0:
+        continue
+    lo, hi = 8, min(n, 200)
+    print(f"CTA {cta}: tiles traced {n}; stats over tiles {lo}..{hi}")
+    for tt in range(2):
+        s = sm[tt][lo:hi]
+        d = np.diff(s, axis=1)
+        print(f"  softmax t={tt}: ld S {med(d[:,0]):.0f}  half0(+max) {med(d[:,1]+d[:,2]):.0f}  half1 {med(d[:,3]):.0f}"
+              f"  | period {med(np.diff(s[:,0])):.0f}  half1 arrive -> next S_FULL {med(s[1:,0]-s[:-1,4]):.0f}")
+    if cta != 0:
+        continue
+    m = a[2560:2560 + 1536].reshape(256, 6)[lo:hi]
+    print(f"  mma period {med(np.diff(m[:,2])):.0f}")
+    for tt in range(2):
+        s = sm[tt][lo:hi]
+        print(f"  t={tt}: own half0 arrive -> issuer wakes {med(m[:,3*tt]-s[:,2]):.0f}"
+              f"  own half1 arrive -> issuer wakes {med(m[:,3*tt+1]-s[:,4]):.0f}"
+              f"  wake h1 -> S(next) issued {med(m[1:,3*tt+2]-m[:-1,3*tt+1]):.0f}"
+              f"  S issued -> S_FULL seen {med(s[:,0]-m[:,3*tt+2]):.0f}")
+# event timeline of CTA 0 for a few consecutive tiles (cycles relative to S0 issue of the first)
+a = A[:4096]
 sm = [a[tt * 1280: tt * 1280 + 1280].reshape(256, 5) for tt in range(2)]
-mm = a[2560:2560 + 1024].reshape(256, 4)
-n = int((sm[0][:, 0] > 0).sum())
-lo, hi = 8, min(n, 200)
-print(f"tiles traced: {n}; stats over tiles {lo}..{hi}")
-for tt in range(2):
-    s = sm[tt][lo:hi]
-    d = np.diff(s, axis=1)
-    print(f"softmax t={tt}: ld S {np.median(d[:,0]):.0f}  max {np.median(d[:,1]):.0f}  exp+stP {np.median(d[:,2]):.0f}"
-          f"  wait/fence/arrive {np.median(d[:,3]):.0f}  | S_FULL->S_FULL period {np.median(np.diff(s[:,0])):.0f}"
-          f"  arrive->next S_FULL {np.median(s[1:,0]-s[:-1,4]):.0f}")
-m = mm[lo:hi]
-print(f"mma: P0 wait->S0 issued {np.median(m[:,1]-m[:,0]):.0f}  P1 wait->S1 issued {np.median(m[:,3]-m[:,2]):.0f}"
-      f"  period {np.median(np.diff(m[:,0])):.0f}")
-# cross-role latencies: softmax arrive (t) -> MMA sees P_FULL(t) for the same tile
-for tt in range(2):
-    lat = m[1:, 2 * tt] - sm[tt][lo:hi - 1, 4]
-    print(f"t={tt}: softmax arrive -> MMA wakes {np.median(lat):.0f};  MMA S issued -> softmax S_FULL {np.median(sm[tt][lo+1:hi,0] - m[:-1, 2*tt+1]):.0f}")
+m = a[2560:2560 + 1536].reshape(256, 6)
+ev = []
+for g in range(100, 104):
+    for tt in range(2):
+        ev += [(m[g, 3*tt+2], f"S{tt}({g}) issued"), (sm[tt][g, 0], f"  S{tt}({g}) FULL seen by softmax{tt}"),
+               (sm[tt][g, 2], f"  P{tt}({g}) h0 arrive"), (sm[tt][g, 4], f"  P{tt}({g}) h1 arrive"),
+               (m[g, 3*tt], f"issuer wakes P{tt}({g}) h0 -> PV h0"), (m[g, 3*tt+1], f"issuer wakes P{tt}({g}) h1 -> PV h1")]
+off = int(A[4096 + 4095]) - int(A[4095])  # peer clock - leader clock at the cluster sync
+sm1 = [A[4096 + tt * 1280: 4096 + tt * 1280 + 1280].reshape(256, 5) - off for tt in range(2)]
+for g in range(100, 104):
+    for tt in range(2):
+        ev += [(sm1[tt][g, 0], f"  [peer] S{tt}({g}) FULL seen"), (sm1[tt][g, 2], f"  [peer] P{tt}({g}) h0 arrive"),
+               (sm1[tt][g, 4], f"  [peer] P{tt}({g}) h1 arrive")]
+print("peer clock offset", off)
+base = m[100, 2]
+for t_, name in sorted(ev):
+    print(f"{t_ - base:7d}  {name}")
+# mean vs median tile period (item boundaries show up in the mean)
+per = np.diff(A[2560:2560 + 1536].reshape(256, 6)[8:250, 2])
+print(f"S0 issue period: median {np.median(per):.0f} mean {per.mean():.0f}; slowest 10: {np.sort(per)[-10:]}")
