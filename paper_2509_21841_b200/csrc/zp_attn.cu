@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int h = 0; h < 2; ++h) {
           mbar_wait(bar(B_PFULL + 2 * t + h), (jg - 1) & 1);
           tc_fence_after();
-          if (lane == 0 && jg < 255) ZP_STAMP(2560 + int(jg - 1) * 6 + 3 * t + h);
+          if (lane == 0 && jg < 200) ZP_STAMP(2560 + int(jg - 1) * 6 + 3 * t + h);
           issue_pv<kPair>(tO[t], tS[t] + 64, v_desc0 + v_step * pvs, idesc_pv, prev_acc, h);
         }
         commit<kPair>(bar(B_ODONE + t));
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int t = 0; t < 2; ++t) {
               issue_qk<kPair>(tS[t], q_desc0 + q_step * t, k_desc0 + k_step * kst, idesc_qk);
               commit<kPair>(bar(B_SFULL + t));
-              if (lane == 0 && jg < 255) ZP_STAMP(2560 + int(jg) * 6 + 3 * t + 2);
+              if (lane == 0 && jg < 200) ZP_STAMP(2560 + int(jg) * 6 + 3 * t + 2);
             }
           } else {
             for (int t = 0; t < 2; ++t) {
@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               issue_qk<kPair>(tS[t], q_desc0 + q_step * t, k_desc0 + k_step * kst, idesc_qk);
               commit<kPair>(bar(B_SFULL + t));
-              if (lane == 0 && jg < 255) ZP_STAMP(2560 + int(jg) * 6 + 3 * t + 2);
+              if (lane == 0 && jg < 200) ZP_STAMP(2560 + int(jg) * 6 + 3 * t + 2);
             }
           }
           if (jg > 0) commit<kPair>(bar(B_VEMPTY + pvs));
@@ -533,14 +533,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t pfull = lead(B_PFULL + 2 * t);  // + 8 bytes: second half
     const float sl2 = args.scale_log2;
     uint32_t jg = 0;
+#ifdef ZP_TRACE
+    // item-level stamps: 3760 + (item * 2 + t) * 4 + {epilogue start, epilogue end, next item claimed, tiles counted}
+    int tri = -4;
+    auto item_stamp = [&](int e) {
+      if (quad == 0 && lane == 0 && tri >= 0 && tri < 41) ZP_STAMP(3760 + (tri * 2 + t) * 4 + e);
+    };
+#else
+    auto item_stamp = [](int) {};
+#endif
     for (uint32_t k = 0;; ++k) {
       const int idx = sched_wait(k);
       __syncwarp();
       if (lane == 0) sched_release(k);
+      item_stamp(2);
       if (idx >= n_units) break;
       const zp_attn_item it = args.items[kPair ? 2 * idx + int(cta) : idx];
       TileCursor cur(args.segs, it.seg_begin, it.seg_count, it.q_pos0 + it.q_len - 1);
       if (count_tiles(args.segs, it) == 0) continue;
+#ifdef ZP_TRACE
+      ++tri;
+#endif
+      item_stamp(3);
       const bool resume = (it.flags & ZP_ITEM_LOAD_STATE) != 0;
       const int h = 2 * it.head_pair + t;
       const int qpos = it.q_pos0 + row;
@@ -740,6 +754,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------- epilogue of this item (overlaps the next item's S MMAs)
       mbar_wait(bar(B_ODONE + t), (jg - 1) & 1);
       tc_fence_after();
+      item_stamp(0);
       if (it.flags & ZP_ITEM_STORE_STATE) {
         const int srow = it.state_row0 + row;
         float4* dst = reinterpret_cast<float4*>(args.st_o + (size_t(srow) * args.hq + h) * kHeadDim);
@@ -786,6 +801,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           args.lse[size_t(h) * args.lse_stride + it.q_row0 + row] = lse;
         }
       }
+      item_stamp(1);
     }
   }
 
