@@ -88,7 +88,8 @@ struct Cfg {
   static constexpr uint32_t kSmemK = 2 * kTileBytes;
   static constexpr uint32_t kSmemV = kSmemK + kKStages * kKBytes;
   static constexpr uint32_t kSmemBar = kSmemV + kVStages * kVBytes;
-  static constexpr uint32_t kSmemBytes = kSmemBar + 512 + 1024;  // barriers/sched ring + alignment slack
+  static constexpr uint32_t kSmemSched = kSmemBar + 512;            // schedule ring: kSchedSlots x SchedSlot
+  static constexpr uint32_t kSmemBytes = kSmemSched + 256 + 1024;  // + alignment slack
   static constexpr uint32_t kPFullCount = kPair ? 8 : 4;          // one arrival per softmax warp (x CTAs)
   static constexpr uint32_t kSchedConsumers = kPair ? 18 : 9;
 };
@@ -131,14 +132,16 @@ struct AttnArgs {
 // item's last visible key (causal pruning; fully-masked tiles never issued).
 struct TileCursor {
   const zp_kv_seg* segs;
-  int s, end, max_qpos, ti, nt;
-  zp_kv_seg g;
+  int s, first, end, max_qpos, ti, nt;
+  zp_kv_seg g, g0;  // g0: segs[first], handed over through the schedule ring
   __device__ __forceinline__ TileCursor(const zp_kv_seg* sg, int b, int c, int mq)
-      : segs(sg), s(b - 1), end(b + c), max_qpos(mq), ti(0), nt(0) {}
+      : segs(sg), s(b - 1), first(-1), end(b + c), max_qpos(mq), ti(0), nt(0) {}
+  __device__ __forceinline__ TileCursor(const zp_kv_seg* sg, int b, int c, int mq, const zp_kv_seg& seg0)
+      : segs(sg), s(b - 1), first(b), end(b + c), max_qpos(mq), ti(0), nt(0), g0(seg0) {}
   __device__ __forceinline__ bool next() {
     if (++ti < nt) return true;
     while (++s < end) {
-      g = segs[s];
+      g = s == first ? g0 : segs[s];
       if (g.len > 0 && g.pos0 <= max_qpos) {
         nt = (min(g.len, max_qpos - g.pos0 + 1) + kBN - 1) / kBN;
         ti = 0;
@@ -277,6 +280,16 @@ __device__ __forceinline__ void issue_pv(uint32_t d_tmem, uint32_t p_tmem, uint6
   }
 }
 
+// One published work unit of the schedule ring: the claimed index plus what
+// every consumer needs to start it without global loads (this CTA's item, its
+// tile count, its first KV segment).
+struct SchedSlot {
+  int idx, n_tiles, pad0, pad1;
+  zp_attn_item item;
+  zp_kv_seg seg0;
+};
+static_assert(sizeof(SchedSlot) == 64, "schedule slot layout");
+
 __device__ __forceinline__ int count_tiles(const zp_kv_seg* segs, const zp_attn_item& it) {
   int n = 0;
   TileCursor cur(segs, it.seg_begin, it.seg_count, it.q_pos0 + it.q_len - 1);
@@ -301,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t bar0 = sbase + C::kSmemBar;
   auto bar = [&](int i) -> uint32_t { return bar0 + 8u * uint32_t(i); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sgen + C::kSmemBar + 8 * B_COUNT);
-  volatile int* ring_idx = reinterpret_cast<volatile int*>(sgen + C::kSmemBar + 8 * B_COUNT + 16);
+  SchedSlot* ring = reinterpret_cast<SchedSlot*>(sgen + C::kSmemSched);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -346,16 +359,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // Next work unit for a consumer: wait for the slot, then release it to the
   // publishing producer (leader's ring in a pair).
-  auto sched_wait = [&](uint32_t k) -> int {
+  auto sched_wait = [&](uint32_t k) -> SchedSlot {
     const uint32_t slot = k % kSchedSlots;
     // the peer CTA's ring is written remotely by the leader: cluster-scope acquire
     if (kPair && cta != 0) mbar_wait_cluster(bar(B_SCHED_FULL + slot), (k / kSchedSlots) & 1);
     else mbar_wait(bar(B_SCHED_FULL + slot), (k / kSchedSlots) & 1);
-    return ring_idx[slot];
+    return ring[slot];
   };
+  // The slot was copied to registers before this arrive (release.cta: the
+  // cluster-scope release of the P hand-off cost ~1,000 cycles per arrive).
   auto sched_release = [&](uint32_t k) {
     const uint32_t slot = k % kSchedSlots;
-    if constexpr (kPair) mbar_arrive_cluster(lead(B_SCHED_EMPTY + slot));
+    if constexpr (kPair) mbar_arrive_remote(lead(B_SCHED_EMPTY + slot));
     else mbar_arrive(bar(B_SCHED_EMPTY + slot));
   };
 
@@ -370,36 +385,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_kv = policy_evict_last();
       uint32_t jg = 0, qn = 0;
       for (uint32_t k = 0;; ++k) {
-        int idx;
+        SchedSlot u;
         if (cta == 0) {
           const uint32_t slot = k % kSchedSlots;
           if (k >= kSchedSlots) {
             if constexpr (kPair) mbar_wait_cluster(bar(B_SCHED_EMPTY + slot), ((k / kSchedSlots) - 1) & 1);
             else mbar_wait(bar(B_SCHED_EMPTY + slot), ((k / kSchedSlots) - 1) & 1);
           }
-          idx = atomicAdd(args.next_unit, 1);
-          ring_idx[slot] = idx;
+          u.idx = atomicAdd(args.next_unit, 1);
+          u.n_tiles = 0;
+          u.pad0 = u.pad1 = 0;
+          zp_attn_item o{};
+          if (u.idx < n_units) {
+            u.item = args.items[kPair ? 2 * u.idx : u.idx];
+            if constexpr (kPair) {
+              // contract: items 2p / 2p+1 are the same tile for head pairs 2g / 2g+1
+              o = args.items[2 * u.idx + 1];
+              const zp_attn_item& it = u.item;
+              if (o.q_row0 != it.q_row0 || o.q_pos0 != it.q_pos0 || o.q_len != it.q_len ||
+                  o.seg_begin != it.seg_begin || o.seg_count != it.seg_count || o.state_row0 != it.state_row0 ||
+                  o.flags != it.flags || it.head_pair != (o.head_pair ^ 1) || (it.head_pair & 1) != 0)
+                __trap();
+            }
+            u.n_tiles = count_tiles(args.segs, u.item);
+            if (u.item.seg_count > 0) u.seg0 = args.segs[u.item.seg_begin];
+          }
+          ring[slot] = u;
           if constexpr (kPair) {
-            const uint32_t peer_idx = mapa_shared(smem_u32(const_cast<int*>(ring_idx + slot)), 1);
-            st_cluster_u32(peer_idx, uint32_t(idx));
+            // the peer CTA's slot: same unit, its own item (head pair 2g+1)
+            const int4* w = reinterpret_cast<const int4*>(&u);
+            const int4* wo = reinterpret_cast<const int4*>(&o);
+            const uint32_t peer = mapa_shared(smem_u32(ring + slot), 1);
+            st_cluster_v4(peer, w[0]);
+            st_cluster_v4(peer + 16, wo[0]);
+            st_cluster_v4(peer + 32, wo[1]);
+            st_cluster_v4(peer + 48, w[3]);
             mbar_arrive_cluster(mapa_shared(bar(B_SCHED_FULL + slot), 1));
           }
           mbar_arrive(bar(B_SCHED_FULL + slot));
         } else {
-          idx = sched_wait(k);
+          u = sched_wait(k);
           sched_release(k);
         }
-        if (idx >= n_units) break;
-        const zp_attn_item it = args.items[kPair ? 2 * idx + int(cta) : idx];
-        if constexpr (kPair) {
-          // contract: items 2p / 2p+1 are the same tile for head pairs 2g / 2g+1
-          const zp_attn_item o = args.items[2 * idx + 1 - int(cta)];
-          if (o.q_row0 != it.q_row0 || o.q_pos0 != it.q_pos0 || o.q_len != it.q_len ||
-              o.seg_begin != it.seg_begin || o.seg_count != it.seg_count || o.state_row0 != it.state_row0 ||
-              o.flags != it.flags || it.head_pair != (o.head_pair ^ 1) || (it.head_pair & 1) != int(cta))
-            __trap();
-        }
-        if (count_tiles(args.segs, it) == 0) continue;
+        if (u.idx >= n_units) break;
+        const zp_attn_item it = u.item;
+        if (u.n_tiles == 0) continue;
         const int kvh = (2 * it.head_pair) / args.group;
         if (qn > 0) mbar_wait(bar(B_QEMPTY), (qn - 1) & 1);
         if (cta == 0) mbar_expect_tx(bar(B_QFULL), (kPair ? 4 : 2) * kTileBytes);
@@ -411,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             else tma_load_2d(dst, &tm_q, bar(B_QFULL), x, it.q_row0, pol_q);
           }
         ++qn;
-        TileCursor cur(args.segs, it.seg_begin, it.seg_count, it.q_pos0 + it.q_len - 1);
+        TileCursor cur(args.segs, it.seg_begin, it.seg_count, it.q_pos0 + it.q_len - 1, u.seg0);
         for (; cur.next(); ++jg) {
           const int kst = int(jg % C::kKStages), vst = int(jg % C::kVStages);
           const uint32_t ku = jg / C::kKStages, vu = jg / C::kVStages;
@@ -465,11 +495,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         commit<kPair>(bar(B_ODONE + t));
       };
       for (uint32_t k = 0;; ++k) {
-        const int idx = __shfl_sync(0xffffffffu, sched_wait(k), 0);
+        const SchedSlot u = sched_wait(k);
+        __syncwarp();
         if (lane == 0) sched_release(k);
-        if (idx >= n_units) break;
-        const zp_attn_item it = args.items[kPair ? 2 * idx : idx];
-        const int n = count_tiles(args.segs, it);
+        if (u.idx >= n_units) break;
+        const zp_attn_item it = u.item;
+        const int n = u.n_tiles;
         if (n == 0) continue;
         const bool resume = (it.flags & ZP_ITEM_LOAD_STATE) != 0;
         for (int j = 0; j < n; ++j, ++jg) {
@@ -543,14 +574,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto item_stamp = [](int) {};
 #endif
     for (uint32_t k = 0;; ++k) {
-      const int idx = sched_wait(k);
+      const SchedSlot u = sched_wait(k);
       __syncwarp();
       if (lane == 0) sched_release(k);
       item_stamp(2);
-      if (idx >= n_units) break;
-      const zp_attn_item it = args.items[kPair ? 2 * idx + int(cta) : idx];
-      TileCursor cur(args.segs, it.seg_begin, it.seg_count, it.q_pos0 + it.q_len - 1);
-      if (count_tiles(args.segs, it) == 0) continue;
+      if (u.idx >= n_units) break;
+      const zp_attn_item it = u.item;
+      TileCursor cur(args.segs, it.seg_begin, it.seg_count, it.q_pos0 + it.q_len - 1, u.seg0);
+      if (u.n_tiles == 0) continue;
 #ifdef ZP_TRACE
       ++tri;
 #endif
@@ -568,18 +599,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           m = args.st_ml[size_t(h) * args.state_rows + srow];
           l = args.st_ml[size_t(args.hq + h) * args.state_rows + srow];
         }
-        const float4* src =
-            reinterpret_cast<const float4*>(args.st_o + (size_t(srow) * args.hq + h) * kHeadDim);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(args.st_o + (size_t(srow) * args.hq + h) * kHeadDim);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t rr[32];
 #pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            float4 x = ok ? src[c * 8 + v] : make_float4(0.f, 0.f, 0.f, 0.f);
-            rr[4 * v + 0] = __float_as_uint(x.x);
-            rr[4 * v + 1] = __float_as_uint(x.y);
-            rr[4 * v + 2] = __float_as_uint(x.z);
-            rr[4 * v + 3] = __float_as_uint(x.w);
+          for (int v = 0; v < 4; ++v) {
+            if (ok) {
+              ldg_v8(src + c * 128 + v * 32, rr + 8 * v);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) rr[8 * v + e] = 0u;
+            }
           }
           tmem_st32(tO + c * 32, rr);
         }
@@ -757,7 +788,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       item_stamp(0);
       if (it.flags & ZP_ITEM_STORE_STATE) {
         const int srow = it.state_row0 + row;
-        float4* dst = reinterpret_cast<float4*>(args.st_o + (size_t(srow) * args.hq + h) * kHeadDim);
+        uint8_t* dst = reinterpret_cast<uint8_t*>(args.st_o + (size_t(srow) * args.hq + h) * kHeadDim);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t rr[32];
@@ -765,10 +796,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_wait_ld();
           if (ok) {
 #pragma unroll
-            for (int v = 0; v < 8; ++v)
-              dst[c * 8 + v] = make_float4(__uint_as_float(rr[4 * v]), __uint_as_float(rr[4 * v + 1]),
-                                           __uint_as_float(rr[4 * v + 2]),
-                                           __uint_as_float(rr[4 * v + 3]));
+            for (int v = 0; v < 4; ++v) stg_v8(dst + c * 128 + v * 32, rr + 8 * v);
           }
         }
         if (ok) {
@@ -777,23 +805,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else {
         const float inv_l = l > 0.f ? 1.f / l : 0.f;
-        uint4* dst = reinterpret_cast<uint4*>(args.o + (size_t(it.q_row0 + row) * args.hq + h) *
-                                                           kHeadDim);
+        // one 256-bit store per 16 dims: full 32-byte sectors of the row
+        uint8_t* dst = reinterpret_cast<uint8_t*>(args.o + (size_t(it.q_row0 + row) * args.hq + h) * kHeadDim);
+        const float2 il2 = make_float2(inv_l, inv_l);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t rr[32];
           tmem_ld32(tO + c * 32, rr);
           tmem_wait_ld();
           if (ok) {
+            uint32_t pk[16];
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              uint4 w;
-              w.x = pack_bf16(__uint_as_float(rr[8 * v + 0]) * inv_l, __uint_as_float(rr[8 * v + 1]) * inv_l);
-              w.y = pack_bf16(__uint_as_float(rr[8 * v + 2]) * inv_l, __uint_as_float(rr[8 * v + 3]) * inv_l);
-              w.z = pack_bf16(__uint_as_float(rr[8 * v + 4]) * inv_l, __uint_as_float(rr[8 * v + 5]) * inv_l);
-              w.w = pack_bf16(__uint_as_float(rr[8 * v + 6]) * inv_l, __uint_as_float(rr[8 * v + 7]) * inv_l);
-              dst[c * 4 + v] = w;
+            for (int v = 0; v < 16; ++v) {
+              const float2 x =
+                  __fmul2_rn(make_float2(__uint_as_float(rr[2 * v]), __uint_as_float(rr[2 * v + 1])), il2);
+              pk[v] = pack_bf16(x.x, x.y);
             }
+            stg_v8(dst + c * 64, pk);
+            stg_v8(dst + c * 64 + 32, pk + 8);
           }
         }
         if (ok) {
