@@ -107,7 +107,9 @@ enum : int {
   B_QEMPTY = 25,
   B_SCHED_FULL = 26,    // +slot (4): item index published by the producer
   B_SCHED_EMPTY = 30,   // +slot (4): consumed by the MMA issuer and the softmax warps
-  B_COUNT = 34
+  B_QFULL1 = 34,        // head tile 1's Q (B_QFULL / B_QEMPTY: head tile 0), so each head's
+  B_QEMPTY1 = 35,       // next Q streams in as soon as that head's last QK^T is done
+  B_COUNT = 36
 };
 static_assert(Cfg<true>::kKStages <= 4 && Cfg<true>::kVStages <= 4, "ring depth <= 4");
 static_assert(Cfg<true>::kSmemBytes <= 232448 && Cfg<false>::kSmemBytes <= 232448, "smem budget");
@@ -326,6 +328,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     mbar_init(bar(B_QFULL), 1);
     mbar_init(bar(B_QEMPTY), 1);
+    mbar_init(bar(B_QFULL1), 1);
+    mbar_init(bar(B_QEMPTY1), 1);
     for (int k = 0; k < kSchedSlots; ++k) {
       mbar_init(bar(B_SCHED_FULL + k), 1);
       mbar_init(bar(B_SCHED_EMPTY + k), C::kSchedConsumers);
@@ -431,18 +435,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const zp_attn_item it = u.item;
         if (u.n_tiles == 0) continue;
         const int kvh = (2 * it.head_pair) / args.group;
-        if (qn > 0) mbar_wait(bar(B_QEMPTY), (qn - 1) & 1);
-        if (cta == 0) mbar_expect_tx(bar(B_QFULL), (kPair ? 4 : 2) * kTileBytes);
-        for (int t = 0; t < 2; ++t)
+        // Q of head tile t, once that head's last QK^T of the previous item is done
+        auto load_q = [&](int t) {
+          const int qf = t ? B_QFULL1 : B_QFULL;
+          if (qn > 0) mbar_wait(bar(t ? B_QEMPTY1 : B_QEMPTY), (qn - 1) & 1);
+          if (cta == 0) mbar_expect_tx(bar(qf), (kPair ? 2 : 1) * kTileBytes);
           for (int b = 0; b < 2; ++b) {
             const uint32_t dst = sbase + C::kSmemQ + t * kTileBytes + b * kBoxBytes;
             const int x = (2 * it.head_pair + t) * kHeadDim + b * 64;
-            if constexpr (kPair) tma_load_2d_pair(dst, &tm_q, lead(B_QFULL), x, it.q_row0, pol_q);
-            else tma_load_2d(dst, &tm_q, bar(B_QFULL), x, it.q_row0, pol_q);
+            if constexpr (kPair) tma_load_2d_pair(dst, &tm_q, lead(qf), x, it.q_row0, pol_q);
+            else tma_load_2d(dst, &tm_q, bar(qf), x, it.q_row0, pol_q);
           }
-        ++qn;
+        };
+        load_q(0);
         TileCursor cur(args.segs, it.seg_begin, it.seg_count, it.q_pos0 + it.q_len - 1, u.seg0);
-        for (; cur.next(); ++jg) {
+        for (int jj = 0; cur.next(); ++jg, ++jj) {
+          if (jj == 1) load_q(1);  // after the first K/V tile: head 1's Q is needed later
           const int kst = int(jg % C::kKStages), vst = int(jg % C::kVStages);
           const uint32_t ku = jg / C::kKStages, vu = jg / C::kVStages;
           const int row = cur.row();
@@ -467,6 +475,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                           kvh * kHeadDim + b * 64, row, pol_kv);
           }
         }
+        if (u.n_tiles == 1) load_q(1);
+        ++qn;
       }
     } else if (warp == 1 && cta == 0) {
       // ---------------- MMA issuer (whole warp; one elected lane issues each
@@ -511,35 +521,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(bar(B_VFULL + pvs), ((jg - 1) / C::kVStages) & 1);
             tc_fence_after();
           }
-          if (j == 0) {
-            // item boundary: finish the previous item's PVs first so its
-            // epilogue is not held up by this item's Q load
-            if (jg > 0) {
-              for (int t = 0; t < 2; ++t) pv_prev(t, pvs);
-            }
-            mbar_wait(bar(B_QFULL), qn & 1);
-            mbar_wait(bar(B_KFULL + kst), kpar);
+          // PV_t of the previous tile (possibly the previous item's last),
+          // then S_t of this tile; at an item start S_t waits for head t's Q
+          for (int t = 0; t < 2; ++t) {
+            if (jg > 0) pv_prev(t, pvs);
+            if (j == 0) mbar_wait(bar(t ? B_QFULL1 : B_QFULL), qn & 1);
+            if (t == 0) mbar_wait(bar(B_KFULL + kst), kpar);
             tc_fence_after();
-            for (int t = 0; t < 2; ++t) {
-              issue_qk<kPair>(tS[t], q_desc0 + q_step * t, k_desc0 + k_step * kst, idesc_qk);
-              commit<kPair>(bar(B_SFULL + t));
-              if (lane == 0 && jg < 200) ZP_STAMP(2560 + int(jg) * 6 + 3 * t + 2);
-            }
-          } else {
-            for (int t = 0; t < 2; ++t) {
-              pv_prev(t, pvs);
-              if (t == 0) {
-                mbar_wait(bar(B_KFULL + kst), kpar);
-                tc_fence_after();
-              }
-              issue_qk<kPair>(tS[t], q_desc0 + q_step * t, k_desc0 + k_step * kst, idesc_qk);
-              commit<kPair>(bar(B_SFULL + t));
-              if (lane == 0 && jg < 200) ZP_STAMP(2560 + int(jg) * 6 + 3 * t + 2);
-            }
+            issue_qk<kPair>(tS[t], q_desc0 + q_step * t, k_desc0 + k_step * kst, idesc_qk);
+            commit<kPair>(bar(B_SFULL + t));
+            if (j == n - 1) commit<kPair>(bar(t ? B_QEMPTY1 : B_QEMPTY));  // Q_t free once this S lands
+            if (lane == 0 && jg < 200) ZP_STAMP(2560 + int(jg) * 6 + 3 * t + 2);
           }
           if (jg > 0) commit<kPair>(bar(B_VEMPTY + pvs));
           commit<kPair>(bar(B_KEMPTY + kst));
-          if (j == n - 1) commit<kPair>(bar(B_QEMPTY));  // Q free once this item's S MMAs land
           prev_acc = resume || j > 0;
         }
         ++qn;
@@ -809,20 +804,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* dst = reinterpret_cast<uint8_t*>(args.o + (size_t(it.q_row0 + row) * args.hq + h) * kHeadDim);
         const float2 il2 = make_float2(inv_l, inv_l);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t rr[32];
-          tmem_ld32(tO + c * 32, rr);
+        for (int cc = 0; cc < 2; ++cc) {
+          uint32_t rr[64];  // two TMEM loads in flight per wait
+          tmem_ld32(tO + cc * 64, *reinterpret_cast<uint32_t(*)[32]>(rr));
+          tmem_ld32(tO + cc * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(rr + 32));
           tmem_wait_ld();
           if (ok) {
-            uint32_t pk[16];
+            uint32_t pk[32];
 #pragma unroll
-            for (int v = 0; v < 16; ++v) {
+            for (int v = 0; v < 32; ++v) {
               const float2 x =
                   __fmul2_rn(make_float2(__uint_as_float(rr[2 * v]), __uint_as_float(rr[2 * v + 1])), il2);
               pk[v] = pack_bf16(x.x, x.y);
             }
-            stg_v8(dst + c * 64, pk);
-            stg_v8(dst + c * 64 + 32, pk + 8);
+#pragma unroll
+            for (int w = 0; w < 4; ++w) stg_v8(dst + cc * 128 + w * 32, pk + 8 * w);
           }
         }
         if (ok) {

@@ -3,7 +3,10 @@ sys.path.insert(0, '.')
 from paper_2509_21841_b200 import ops
 from paper_2509_21841_b200.worklist import build_worklist
 # seed-0 github-like 64K batch stand-in: a few long sequences
-for seqlens in ([65536], [32768, 16384, 8192, 8192], [4096]*16):
+import os
+from paper_2509_21841_b200 import workloads as W
+c2 = [n for _, n in W.c2_batch("github", 0).sequences]
+for seqlens in ([65536], [32768, 16384, 8192, 8192], [4096]*16, c2):
     t = sum(seqlens)
     q = torch.randn(t, 32, 128, device='cuda', dtype=torch.bfloat16)
     k = torch.randn(t, 8, 128, device='cuda', dtype=torch.bfloat16)
