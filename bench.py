@@ -277,6 +277,10 @@ def run_gpu(args):
             "remap_rows_moved": moved,
             "l2": "inputs larger than L2 (q/k/v %.0f MB per GPU > 126 MB)" % (rows * (hq + 2 * hkv) * d * 2 / 1e6),
             "parallelism": f"zeppelin plan over {world} GPU(s), one process per GPU",
+            "attention_pairs_per_gpu": sum(r[2] for r in per_rank) / world,
+            "scaling_note": ("BASELINE config 2 at N=1 (all-local 64K batch); config 3 at N>1 puts a 128K "
+                             "sequence in the batch, ~3x the attention pairs per GPU of config 2, so compare "
+                             "roofline.aggregate_tflops across N rather than tokens/s"),
         },
         "roofline": {
             "bound": "tensor",
