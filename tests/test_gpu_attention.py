@@ -41,11 +41,14 @@ def make_qkv(t, hq=32, hkv=8, seed=0):
 
 @pytest.mark.parametrize("seqlens,qscale", [([128], 1.0), ([1], 1.0), ([77], 1.0), ([300, 5, 129, 1000], 1.0),
                                             ([2048, 17, 640], 1.0), ([0, 64, 0, 129, 0], 1.0), ([8192], 1.0),
-                                            ([3000, 700], 6.0), ([1500], 0.05)])
+                                            ([3000, 700], 6.0), ([1500], 0.05),
+                                            ([100] * 64 + [257] * 8, 1.0)])
 def test_varlen_local_matches_fp32(seqlens, qscale):
     """Ragged / empty / long sequences; qscale 6 makes the running max move by
     more than the lazy threshold many times (rescale and speculative-exp
-    fallback paths), 0.05 makes the softmax nearly flat."""
+    fallback paths), 0.05 makes the softmax nearly flat; 64 x 100 + 8 x 257 runs
+    hundreds of back-to-back one- and three-tile items through the schedule ring
+    and the per-head Q barriers."""
     t = sum(seqlens)
     q, k, v = make_qkv(t, seed=len(seqlens))
     q = (q.float() * qscale).to(torch.bfloat16)
