@@ -842,496 +842,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 
-// ============================================================================
-// v2: CTA pair, 64-key tiles, S double-buffered per head.
-//
-// The v1 pipeline keeps one S buffer per head (TMEM is full: 2 x S128 + 2 x
-// O128), so a head's next QK^T can only start after its P has been consumed:
-// the softmax waits for PV + QK^T of its own head every tile (measured: the
-// softmax warps idle ~43% on S_FULL, tensor pipe 70% active).  With 64-key
-// tiles the same 512 columns hold S_{t,0}, S_{t,1} (64 each) per head plus
-// O_t, so the MMA issuer runs one tile ahead: at step g it issues PV(g-2)
-// (whose P aliases the buffer) and then S(g) into the freed buffer, while the
-// softmax works on S(g-1).  Q is double-buffered across items, so the next
-// item's first QK^T also overlaps the current item's last softmax.
-namespace v2 {
-
-constexpr int kBN = 64;
-constexpr int kStages = 4;
-constexpr uint32_t kQTile = 128 * 128 * 2;  // 32 KB (one head, 128 rows)
-constexpr uint32_t kQBox = 128 * 64 * 2;    // 16 KB
-constexpr uint32_t kKBox = 32 * 64 * 2;     // 4 KB: 64 dims x this CTA's 32 keys
-constexpr uint32_t kKStage = 2 * kKBox;     // 8 KB
-constexpr uint32_t kVStage = 64 * 64 * 2;   // 8 KB: 64 keys x this CTA's 64 dims
-constexpr uint32_t kSmemQ = 0;              // [q buffer][head] x 32 KB
-constexpr uint32_t kSmemK = 4 * kQTile;
-constexpr uint32_t kSmemV = kSmemK + kStages * kKStage;
-constexpr uint32_t kSmemBar = kSmemV + kStages * kVStage;
-constexpr uint32_t kSmemBytes = kSmemBar + 512 + 1024;
-static_assert(kSmemBytes <= 232448, "smem budget");
-
-enum : int {
-  B_QFULL = 0,         // +q buffer
-  B_QEMPTY = 2,        // +q buffer
-  B_KFULL = 4,         // +stage
-  B_KEMPTY = 8,        // +stage
-  B_VFULL = 12,        // +stage
-  B_VEMPTY = 16,       // +stage
-  B_SFULL = 20,        // +2*head+buffer
-  B_PFULL = 24,        // +2*head+buffer
-  B_ODONE = 28,        // +head: one completion per PV of that head
-  B_OFREE = 30,        // +head: one completion per item (O drained / resume state loaded)
-  B_SCHED_FULL = 32,   // +slot
-  B_SCHED_EMPTY = 36,  // +slot
-  B_COUNT = 40
-};
-
-struct Cursor64 {
-  const zp_kv_seg* segs;
-  int s, end, max_qpos, ti, nt;
-  zp_kv_seg g;
-  __device__ __forceinline__ Cursor64(const zp_kv_seg* sg, int b, int c, int mq)
-      : segs(sg), s(b - 1), end(b + c), max_qpos(mq), ti(0), nt(0) {}
-  __device__ __forceinline__ bool next() {
-    if (++ti < nt) return true;
-    while (++s < end) {
-      g = segs[s];
-      if (g.len > 0 && g.pos0 <= max_qpos) {
-        nt = (min(g.len, max_qpos - g.pos0 + 1) + kBN - 1) / kBN;
-        ti = 0;
-        return true;
-      }
-    }
-    return false;
-  }
-  __device__ __forceinline__ int row() const { return g.row0 + ti * kBN; }
-  __device__ __forceinline__ int pos() const { return g.pos0 + ti * kBN; }
-  __device__ __forceinline__ int valid() const { return min(kBN, g.len - ti * kBN); }
-};
-
-__device__ __forceinline__ int tiles_of(const zp_kv_seg* segs, const zp_attn_item& it) {
-  int n = 0;
-  Cursor64 cur(segs, it.seg_begin, it.seg_count, it.q_pos0 + it.q_len - 1);
-  while (cur.next()) ++n;
-  return n;
-}
-
-__global__ void __launch_bounds__(kThreads, 1)
-    attn_fwd_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                       const __grid_constant__ CUtensorMap tm_v, const AttnArgs args) {
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw = smem_u32(smem_raw);
-  const uint32_t sbase = (raw + 1023u) & ~1023u;
-  uint8_t* sgen = smem_raw + (sbase - raw);
-  const uint32_t bar0 = sbase + kSmemBar;
-  auto bar = [&](int i) -> uint32_t { return bar0 + 8u * uint32_t(i); };
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sgen + kSmemBar + 8 * B_COUNT);
-  volatile int* ring_idx = reinterpret_cast<volatile int*>(sgen + kSmemBar + 8 * B_COUNT + 16);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int n_units = args.n_units;
-  const uint32_t cta = cluster_ctarank();
-  auto lead = [&](int i) -> uint32_t { return mapa_shared(bar(i), 0); };
-
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(bar(B_QFULL + b), 1);
-      mbar_init(bar(B_QEMPTY + b), 1);
-      mbar_init(bar(B_ODONE + b), 1);
-      mbar_init(bar(B_OFREE + b), 8);
-    }
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(bar(B_KFULL + s), 1);
-      mbar_init(bar(B_KEMPTY + s), 1);
-      mbar_init(bar(B_VFULL + s), 1);
-      mbar_init(bar(B_VEMPTY + s), 1);
-    }
-    for (int i = 0; i < 4; ++i) {
-      mbar_init(bar(B_SFULL + i), 1);
-      mbar_init(bar(B_PFULL + i), 8);  // 4 softmax warps x 2 CTAs
-    }
-    for (int k = 0; k < kSchedSlots; ++k) {
-      mbar_init(bar(B_SCHED_FULL + k), 1);
-      mbar_init(bar(B_SCHED_EMPTY + k), 18);
-    }
-    fence_mbar_init();
-  }
-  if (warp == 1) tmem_alloc_pair(smem_u32(tmem_slot), 512);
-  tc_fence_before();
-  cluster_sync_all();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  auto sched_wait = [&](uint32_t k) -> int {
-    const uint32_t slot = k % kSchedSlots;
-    if (cta != 0) mbar_wait_cluster(bar(B_SCHED_FULL + slot), (k / kSchedSlots) & 1);
-    else mbar_wait(bar(B_SCHED_FULL + slot), (k / kSchedSlots) & 1);
-    return ring_idx[slot];
-  };
-  auto sched_release = [&](uint32_t k) { mbar_arrive_cluster(lead(B_SCHED_EMPTY + (k % kSchedSlots))); };
-
-  if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(ZP_WG0_REGS));
-    if (warp == 0 && lane == 0) {
-      // ---------------- producer
-      tma_prefetch_desc(&tm_q);
-      tma_prefetch_desc(&tm_k);
-      tma_prefetch_desc(&tm_v);
-      const uint64_t pol_q = policy_evict_first();
-      const uint64_t pol_kv = policy_evict_last();
-      uint32_t jg = 0, qn = 0;
-      for (uint32_t k = 0;; ++k) {
-        int idx;
-        if (cta == 0) {
-          const uint32_t slot = k % kSchedSlots;
-          if (k >= kSchedSlots) mbar_wait_cluster(bar(B_SCHED_EMPTY + slot), ((k / kSchedSlots) - 1) & 1);
-          idx = atomicAdd(args.next_unit, 1);
-          ring_idx[slot] = idx;
-          st_cluster_u32(mapa_shared(smem_u32(const_cast<int*>(ring_idx + slot)), 1), uint32_t(idx));
-          mbar_arrive_cluster(mapa_shared(bar(B_SCHED_FULL + slot), 1));
-          mbar_arrive(bar(B_SCHED_FULL + slot));
-        } else {
-          idx = sched_wait(k);
-          sched_release(k);
-        }
-        if (idx >= n_units) break;
-        const zp_attn_item it = args.items[2 * idx + int(cta)];
-        if (tiles_of(args.segs, it) == 0) continue;
-        const int kvh = (2 * it.head_pair) / args.group;
-        const int qb = int(qn & 1);
-        if (qn >= 2) mbar_wait(bar(B_QEMPTY + qb), ((qn >> 1) - 1) & 1);
-        if (cta == 0) mbar_expect_tx(bar(B_QFULL + qb), 4 * kQTile);
-        for (int t = 0; t < 2; ++t)
-          for (int b = 0; b < 2; ++b)
-            tma_load_2d_pair(sbase + kSmemQ + (2 * qb + t) * kQTile + b * kQBox, &tm_q, lead(B_QFULL + qb),
-                             (2 * it.head_pair + t) * kHeadDim + b * 64, it.q_row0, pol_q);
-        ++qn;
-        Cursor64 cur(args.segs, it.seg_begin, it.seg_count, it.q_pos0 + it.q_len - 1);
-        for (; cur.next(); ++jg) {
-          const int st = int(jg % kStages);
-          const uint32_t u = jg / kStages;
-          const int row = cur.row();
-          if (jg >= uint32_t(kStages)) mbar_wait(bar(B_KEMPTY + st), (u - 1) & 1);
-          if (cta == 0) mbar_expect_tx(bar(B_KFULL + st), 2 * kKStage);
-          for (int b = 0; b < 2; ++b)
-            tma_load_2d_pair(sbase + kSmemK + st * kKStage + b * kKBox, &tm_k, lead(B_KFULL + st),
-                             kvh * kHeadDim + b * 64, row + int(cta) * (kBN / 2), pol_kv);
-          if (jg >= uint32_t(kStages)) mbar_wait(bar(B_VEMPTY + st), (u - 1) & 1);
-          if (cta == 0) mbar_expect_tx(bar(B_VFULL + st), 2 * kVStage);
-          tma_load_2d_pair(sbase + kSmemV + st * kVStage, &tm_v, lead(B_VFULL + st),
-                           kvh * kHeadDim + int(cta) * 64, row, pol_kv);
-        }
-      }
-    } else if (warp == 1 && cta == 0) {
-      // ---------------- MMA issuer (leader; the whole warp runs the loop,
-      // one elected lane issues).  Step g: PV(g-2) for both heads, then S(g)
-      // into the buffer PV(g-2) just consumed.
-      constexpr uint32_t idesc_s = idesc_bf16_f32(256, kBN, 0, 0);
-      constexpr uint32_t idesc_pv = idesc_bf16_f32(256, 128, 0, 1);
-      const uint64_t q_desc0 = umma_desc_sw128(sbase + kSmemQ, 16, 1024);
-      const uint64_t k_desc0 = umma_desc_sw128(sbase + kSmemK, 16, 1024);
-      const uint64_t v_desc0 = umma_desc_sw128(sbase + kSmemV, kQBox, 1024);
-      // pending PV info for tiles g-1, g-2 (indexed by tile parity)
-      bool pv_valid[2] = {false, false}, pv_acc[2] = {false, false}, pv_first[2] = {false, false};
-      uint32_t pv_item[2] = {0, 0};
-      uint32_t k_sched = 0, qn = 0, item_no = 0;
-      int cur_n = 0, cur_j = 0, cur_qb = 0;
-      bool cur_resume = false, done_s = false;
-      for (uint32_t g = 0;; ++g) {
-        const int b = int(g & 1);
-        if (g >= 2 && pv_valid[b]) {
-          const int vs = int((g - 2) % kStages);
-          mbar_wait(bar(B_VFULL + vs), ((g - 2) / kStages) & 1);
-          tc_fence_after();
-#pragma unroll 1
-          for (int t = 0; t < 2; ++t) {
-            mbar_wait(bar(B_PFULL + 2 * t + b), ((g - 2) >> 1) & 1);
-            if (lane == 0 && t == 0 && g < 258) ZP_STAMP(2560 + int(g - 2) * 4 + 0);
-            if (pv_first[b]) mbar_wait(bar(B_OFREE + t), pv_item[b] & 1);
-            tc_fence_after();
-            const uint32_t tp = tmem + uint32_t((2 * t + b) * 64 + 32);
-            const uint32_t to = tmem + 256u + uint32_t(128 * t);
-#pragma unroll
-            for (int kk = 0; kk < kBN / 16; ++kk)
-              mma_ts_pair_w(to, tp + kk * 8, v_desc0 + uint64_t(vs * (kVStage >> 4)) + uint64_t(kk * (2048 >> 4)),
-                            idesc_pv, (pv_acc[b] || kk > 0) ? 1u : 0u);
-            tc_commit_pair_w(bar(B_ODONE + t), 0x3);
-          }
-          tc_commit_pair_w(bar(B_VEMPTY + vs), 0x3);
-          pv_valid[b] = false;
-        }
-        if (!done_s && cur_j == cur_n) {
-          // next item with at least one tile
-          for (;;) {
-            const int idx = __shfl_sync(0xffffffffu, sched_wait(k_sched), 0);
-            if (lane == 0) sched_release(k_sched);
-            ++k_sched;
-            if (idx >= n_units) {
-              done_s = true;
-              break;
-            }
-            const zp_attn_item it = args.items[2 * idx];
-            const int n = tiles_of(args.segs, it);
-            if (n == 0) continue;
-            cur_n = n;
-            cur_j = 0;
-            cur_qb = int(qn & 1);
-            item_no = qn;
-            ++qn;
-            cur_resume = (it.flags & ZP_ITEM_LOAD_STATE) != 0;
-            break;
-          }
-        }
-        if (!done_s) {
-          const int ks = int(g % kStages);
-          mbar_wait(bar(B_KFULL + ks), (g / kStages) & 1);
-          if (cur_j == 0) mbar_wait(bar(B_QFULL + cur_qb), (item_no >> 1) & 1);
-          tc_fence_after();
-#pragma unroll 1
-          for (int t = 0; t < 2; ++t) {
-            const uint32_t ts = tmem + uint32_t((2 * t + b) * 64);
-            const uint64_t qd = q_desc0 + uint64_t(((2 * cur_qb + t) * kQTile) >> 4);
-            const uint64_t kd = k_desc0 + uint64_t((ks * kKStage) >> 4);
-#pragma unroll
-            for (int kk = 0; kk < kHeadDim / 16; ++kk) {
-              const uint64_t qo = ((kk >> 2) * kQBox + (kk & 3) * 32) >> 4;
-              const uint64_t ko = ((kk >> 2) * kKBox + (kk & 3) * 32) >> 4;
-              mma_ss_pair_w(ts, qd + qo, kd + ko, idesc_s, kk > 0 ? 1u : 0u);
-            }
-            tc_commit_pair_w(bar(B_SFULL + 2 * t + b), 0x3);
-          }
-          tc_commit_pair_w(bar(B_KEMPTY + ks), 0x3);
-          if (lane == 0 && g < 256) ZP_STAMP(2560 + int(g) * 4 + 1);
-          if (cur_j == cur_n - 1) tc_commit_pair_w(bar(B_QEMPTY + cur_qb), 0x3);
-          pv_valid[b] = true;
-          pv_acc[b] = cur_resume || cur_j > 0;
-          pv_first[b] = cur_j == 0;
-          pv_item[b] = item_no;
-          ++cur_j;
-        } else if (!pv_valid[0] && !pv_valid[1]) {
-          break;
-        }
-      }
-    }
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
-    // ---------------- softmax / correction / epilogue (thread == row)
-    const int t = (warp - 4) >> 2;
-    const int quad = warp & 3;
-    const int row = quad * 32 + lane;
-    const uint32_t lane_bits = uint32_t(quad * 32) << 16;
-    const uint32_t tO = tmem + lane_bits + 256u + uint32_t(t * 128);
-    const float sl2 = args.scale_log2;
-    uint32_t jg = 0;
-    for (uint32_t k = 0;; ++k) {
-      const int idx = sched_wait(k);
-      __syncwarp();
-      if (lane == 0) sched_release(k);
-      if (idx >= n_units) break;
-      const zp_attn_item it = args.items[2 * idx + int(cta)];
-      const int n = tiles_of(args.segs, it);
-      if (n == 0) continue;
-      const bool resume = (it.flags & ZP_ITEM_LOAD_STATE) != 0;
-      const int h = 2 * it.head_pair + t;
-      const int qpos = it.q_pos0 + row;
-      const bool ok = row < it.q_len;
-      float m = -INFINITY, l = 0.f;
-      if (resume) {
-        // O_t is free: this thread's previous epilogue drained it
-        const int srow = it.state_row0 + row;
-        if (ok) {
-          m = args.st_ml[size_t(h) * args.state_rows + srow];
-          l = args.st_ml[size_t(args.hq + h) * args.state_rows + srow];
-        }
-        const float4* src =
-            reinterpret_cast<const float4*>(args.st_o + (size_t(srow) * args.hq + h) * kHeadDim);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t rr[32];
-#pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            float4 x = ok ? src[c * 8 + v] : make_float4(0.f, 0.f, 0.f, 0.f);
-            rr[4 * v + 0] = __float_as_uint(x.x);
-            rr[4 * v + 1] = __float_as_uint(x.y);
-            rr[4 * v + 2] = __float_as_uint(x.z);
-            rr[4 * v + 3] = __float_as_uint(x.w);
-          }
-          tmem_st32(tO + c * 32, rr);
-        }
-        tmem_wait_st();
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_remote(lead(B_OFREE + t));
-
-      Cursor64 cur(args.segs, it.seg_begin, it.seg_count, it.q_pos0 + it.q_len - 1);
-      for (int j = 0; cur.next(); ++j, ++jg) {
-        const int b = int(jg & 1);
-        const uint32_t tS = tmem + lane_bits + uint32_t((2 * t + b) * 64);
-        const int tr = (lane == 0 && quad == 0 && jg < 256) ? t * 1280 + int(jg) * 5 : -1;
-        ZP_STAMP(tr);
-        mbar_wait(bar(B_SFULL + 2 * t + b), (jg >> 1) & 1);
-        tc_fence_after();
-        ZP_STAMP(tr < 0 ? -1 : tr + 1);
-        float s[64];
-        {
-          uint32_t r0[32], r1[32];
-          tmem_ld32(tS, r0);
-          tmem_ld32(tS + 32, r1);
-          tmem_wait_ld();
-#pragma unroll
-          for (int v = 0; v < 32; ++v) {
-            s[v] = __uint_as_float(r0[v]);
-            s[32 + v] = __uint_as_float(r1[v]);
-          }
-        }
-#ifdef ZP_DEBUG_TRIVIAL_SOFTMAX
-        {  // diagnostic build only: measures the MMA pipeline alone
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_remote(lead(B_PFULL + 2 * t + b));
-          if (j == n - 1) mbar_wait(bar(B_ODONE + t), (jg - 1) & 1);
-          continue;
-        }
-#endif
-        const int kpos0 = cur.pos();
-        const int kv_valid = cur.valid();
-        if (kv_valid < kBN || kpos0 + kBN - 1 > it.q_pos0) {
-          const int lim = min(kv_valid - 1, qpos - kpos0);  // last visible column
-#pragma unroll
-          for (int c = 0; c < kBN; ++c)
-            if (c > lim) s[c] = -INFINITY;
-        }
-        float mx0 = fmax3(s[0], s[1], s[2]), mx1 = fmax3(s[3], s[4], s[5]);
-        float mx2 = fmax3(s[6], s[7], s[8]), mx3 = fmax3(s[9], s[10], s[11]);
-#pragma unroll
-        for (int c = 12; c < 60; c += 8) {
-          mx0 = fmax3(mx0, s[c], s[c + 1]);
-          mx1 = fmax3(mx1, s[c + 2], s[c + 3]);
-          mx2 = fmax3(mx2, s[c + 4], s[c + 5]);
-          mx3 = fmax3(mx3, s[c + 6], s[c + 7]);
-        }
-        mx0 = fmax3(mx0, s[60], s[61]);
-        mx1 = fmax3(mx1, s[62], s[63]);
-        const float mx = fmax3(mx0, mx1, fmaxf(mx2, mx3)) * sl2;
-#ifdef ZP_TRACE
-        asm volatile("" ::"f"(mx));
-        ZP_STAMP(tr < 0 ? -1 : tr + 2);
-#endif
-        const bool bump = mx > m + kRescaleLog2;
-        const float m_new = bump ? mx : m;
-        const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-        const float alpha = bump ? ex2(m - m_use) : 1.f;
-        if ((j > 0 || resume) && __any_sync(0xffffffffu, bump)) {
-          if (j > 0) {
-            mbar_wait(bar(B_ODONE + t), (jg - 1) & 1);  // PV of the previous tile landed
-            tc_fence_after();
-          }
-          const float2 a2 = make_float2(alpha, alpha);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t rr[32];
-            tmem_ld32(tO + c * 32, rr);
-            tmem_wait_ld();
-#pragma unroll
-            for (int v = 0; v < 16; ++v) {
-              const float2 o2 =
-                  __fmul2_rn(make_float2(__uint_as_float(rr[2 * v]), __uint_as_float(rr[2 * v + 1])), a2);
-              rr[2 * v] = __float_as_uint(o2.x);
-              rr[2 * v + 1] = __float_as_uint(o2.y);
-            }
-            tmem_st32(tO + c * 32, rr);
-          }
-        }
-        const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m_use, -m_use);
-        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int v = 0; v < 16; ++v) {
-            const float2 x = __ffma2_rn(make_float2(s[c * 32 + 2 * v], s[c * 32 + 2 * v + 1]), sl2x2, negm);
-            float2 p;
-            p.x = ex2(x.x);
-            p.y = ex2(x.y);
-            if (v & 1) acc1 = __fadd2_rn(acc1, p); else acc0 = __fadd2_rn(acc0, p);
-            pk[v] = pack_bf16(p.x, p.y);
-          }
-          tmem_st16(tS + 32 + c * 16, pk);
-        }
-        const float2 acc = __fadd2_rn(acc0, acc1);
-        l = l * alpha + (acc.x + acc.y);
-        m = m_new;
-        // Before handing over the item's last P, make sure the previous PV has
-        // landed: the epilogue then waits ODONE phases strictly in order.
-        if (j == n - 1 && jg > 0) mbar_wait(bar(B_ODONE + t), (jg - 1) & 1);
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_remote(lead(B_PFULL + 2 * t + b));
-        ZP_STAMP(tr < 0 ? -1 : tr + 3);
-      }
-
-      // ---------------- epilogue
-      mbar_wait(bar(B_ODONE + t), (jg - 1) & 1);
-      tc_fence_after();
-      if (it.flags & ZP_ITEM_STORE_STATE) {
-        const int srow = it.state_row0 + row;
-        float4* dst = reinterpret_cast<float4*>(args.st_o + (size_t(srow) * args.hq + h) * kHeadDim);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t rr[32];
-          tmem_ld32(tO + c * 32, rr);
-          tmem_wait_ld();
-          if (ok) {
-#pragma unroll
-            for (int v = 0; v < 8; ++v)
-              dst[c * 8 + v] = make_float4(__uint_as_float(rr[4 * v]), __uint_as_float(rr[4 * v + 1]),
-                                           __uint_as_float(rr[4 * v + 2]), __uint_as_float(rr[4 * v + 3]));
-          }
-        }
-        if (ok) {
-          args.st_ml[size_t(h) * args.state_rows + srow] = m;
-          args.st_ml[size_t(args.hq + h) * args.state_rows + srow] = l;
-        }
-      } else {
-        const float inv_l = l > 0.f ? 1.f / l : 0.f;
-        uint4* dst =
-            reinterpret_cast<uint4*>(args.o + (size_t(it.q_row0 + row) * args.hq + h) * kHeadDim);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t rr[32];
-          tmem_ld32(tO + c * 32, rr);
-          tmem_wait_ld();
-          if (ok) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              uint4 w;
-              w.x = pack_bf16(__uint_as_float(rr[8 * v + 0]) * inv_l, __uint_as_float(rr[8 * v + 1]) * inv_l);
-              w.y = pack_bf16(__uint_as_float(rr[8 * v + 2]) * inv_l, __uint_as_float(rr[8 * v + 3]) * inv_l);
-              w.z = pack_bf16(__uint_as_float(rr[8 * v + 4]) * inv_l, __uint_as_float(rr[8 * v + 5]) * inv_l);
-              w.w = pack_bf16(__uint_as_float(rr[8 * v + 6]) * inv_l, __uint_as_float(rr[8 * v + 7]) * inv_l);
-              dst[c * 4 + v] = w;
-            }
-          }
-        }
-        if (ok) {
-          const float lse = l > 0.f ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
-          args.lse[size_t(h) * args.lse_stride + it.q_row0 + row] = lse;
-        }
-      }
-    }
-  }
-
-  __syncwarp();
-  tc_fence_before();
-  cluster_sync_all();
-  tc_fence_after();
-  if (warp == 1) tmem_dealloc_pair(tmem, 512);
-}
-
-}  // namespace v2
 
 }  // namespace zp
 
@@ -1340,23 +850,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 namespace {
 
-// ZP_ATTN_VARIANT (A/B measurements only): "single" = one-CTA kernel,
-// "v2" = 64-key double-buffered-S pair kernel; default = CTA pair, 128-key tiles.
+// ZP_ATTN_VARIANT (A/B measurements only): "single" = one-CTA kernel;
+// default = CTA pair (when the GQA group allows it).
 int variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("ZP_ATTN_VARIANT");
-    v = !e ? 1 : (e[0] == 's' ? 0 : (e[0] == 'v' ? 2 : 1));
+    v = !e ? 1 : (e[0] == 's' ? 0 : 1);
   }
   return v;
 }
 
-template <bool kPair, bool kV2 = false>
+template <bool kPair>
 int launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, zp::AttnArgs a,
                 int n_units, cudaStream_t stream) {
   using namespace zp;
-  constexpr uint32_t smem = kV2 ? v2::kSmemBytes : Cfg<kPair>::kSmemBytes;
-  auto kernel = kV2 ? v2::attn_fwd_v2_kernel : attn_fwd_kernel<kPair>;
+  constexpr uint32_t smem = Cfg<kPair>::kSmemBytes;
+  auto kernel = attn_fwd_kernel<kPair>;
   static bool attr_done = false;
   static int max_units = 0;  // resident CTAs (single) or CTA pairs (pair)
   if (!attr_done) {
@@ -1440,17 +950,16 @@ extern "C" int zp_attn_fwd(const void* q, const void* k, const void* v, int q_ro
   // (GQA group a multiple of 4) and the item list in aligned pairs.
   const int var = variant();
   const bool pair = (hq / hkv) % 4 == 0 && n_items % 2 == 0 && var != 0;
-  const bool v2 = pair && var == 2;
   CUtensorMap tq, tk, tv;
   int rc;
   if ((rc = zp_make_tmap_2d_bf16(&tq, q, uint64_t(hq) * kHeadDim, uint64_t(q_rows),
                                  uint64_t(hq) * kHeadDim * 2, 64, 128)) != ZP_OK)
     return rc;
   if ((rc = zp_make_tmap_2d_bf16(&tk, k, uint64_t(hkv) * kHeadDim, uint64_t(kv_rows),
-                                 uint64_t(kv_row_stride) * 2, 64, v2 ? 32 : (pair ? 64 : 128))) != ZP_OK)
+                                 uint64_t(kv_row_stride) * 2, 64, pair ? 64 : 128)) != ZP_OK)
     return rc;
   if ((rc = zp_make_tmap_2d_bf16(&tv, v, uint64_t(hkv) * kHeadDim, uint64_t(kv_rows),
-                                 uint64_t(kv_row_stride) * 2, 64, v2 ? 64 : 128)) != ZP_OK)
+                                 uint64_t(kv_row_stride) * 2, 64, 128)) != ZP_OK)
     return rc;
 
   AttnArgs a;
@@ -1469,7 +978,6 @@ extern "C" int zp_attn_fwd(const void* q, const void* k, const void* v, int q_ro
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t me = cudaMemsetAsync(workspace, 0, sizeof(int), s);
   if (me != cudaSuccess) return zp_fail_cuda(me, "zp_attn_fwd: workspace reset");
-  if (v2) return launch_attn<true, true>(tq, tk, tv, a, n_items / 2, s);
   return pair ? launch_attn<true>(tq, tk, tv, a, n_items / 2, s)
               : launch_attn<false>(tq, tk, tv, a, n_items, s);
 }
