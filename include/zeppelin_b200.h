@@ -220,6 +220,12 @@ ZP_API int zp_ipc_get_handle(void* dev_ptr, void* handle_out64, int64_t* offset_
 ZP_API int zp_ipc_open_handle(const void* handle64, void** dev_ptr_out);
 ZP_API int zp_ipc_close_handle(void* dev_ptr);
 
+/* SMs the persistent attention launches leave free (rounded up to whole CTA
+ * pairs), process-wide; 0 (default) = every SM.  Ring rounds set it while a
+ * KV hop is in flight so the communication kernels (NCCL P2P) are not queued
+ * behind a kernel that holds every SM.  Returns the previous value. */
+ZP_API int zp_attn_set_sm_reserve(int sms);
+
 /* Misc. */
 ZP_API const char* zp_last_error(void);
 ZP_API int zp_device_sm_count(void);

@@ -43,6 +43,7 @@ SIGNATURES: dict[str, tuple] = {
     "zp_ipc_get_handle": (_c_int, [_vp, _vp, ctypes.POINTER(_c_i64)]),
     "zp_ipc_open_handle": (_c_int, [_vp, ctypes.POINTER(_vp)]),
     "zp_ipc_close_handle": (_c_int, [_vp]),
+    "zp_attn_set_sm_reserve": (_c_int, [_c_int]),
     "zp_last_error": (ctypes.c_char_p, []),
     "zp_device_sm_count": (_c_int, []),
     "zp_version": (_c_int, []),

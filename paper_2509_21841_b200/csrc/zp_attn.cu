@@ -850,6 +850,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 namespace {
 
+int g_sm_reserve = 0;  // zp_attn_set_sm_reserve
+
 // ZP_ATTN_VARIANT (A/B measurements only): "single" = one-CTA kernel;
 // default = CTA pair (when the GQA group allows it).
 int variant() {
@@ -898,7 +900,11 @@ int launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap&
     attr_done = true;
   }
   a.n_units = n_units;
-  const int units = n_units < max_units ? n_units : max_units;  // persistent
+  // persistent; g_sm_reserve SMs (whole units) stay free for concurrent comm kernels
+  const int per_unit = kPair ? 2 : 1;
+  int cap = max_units - (g_sm_reserve + per_unit - 1) / per_unit;
+  if (cap < 1) cap = 1;
+  const int units = n_units < cap ? n_units : cap;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
   cfg.blockDim = dim3(kThreads);
@@ -928,6 +934,12 @@ extern "C" ZP_API int zp_debug_trace(unsigned long long* host, int n) {
                  cudaSuccess ? 0 : -1;
 }
 #endif
+
+extern "C" int zp_attn_set_sm_reserve(int sms) {
+  const int prev = g_sm_reserve;
+  g_sm_reserve = sms < 0 ? 0 : sms;
+  return prev;
+}
 
 extern "C" int zp_attn_fwd(const void* q, const void* k, const void* v, int q_rows, int kv_rows,
                            int kv_row_stride, int hq, int hkv, int head_dim, void* o, float* lse,

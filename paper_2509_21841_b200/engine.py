@@ -25,9 +25,11 @@ Public entry points (drop-in execution of what the reference only costs):
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
+
 import torch
 import torch.distributed as dist
 
@@ -37,6 +39,14 @@ from .program import BwdProgram, RankProgram, build_bwd_program, build_rank_prog
 from .remap import RemapLayout, remap_layout
 from .schedule import build_schedule
 from .worklist import BwdWorkList, WorkList
+
+
+# SMs a ring round's attention launch leaves free while the next KV hop is in
+# flight, and the CTA cap of the ring communicator: NCCL's P2P kernels need
+# SMs, and a persistent kernel holding all of them queues the hop behind the
+# whole round.  Measured at N=4 (C3): step 52.7 -> 50.8 ms with 4 SMs / 2 CTAs.
+RING_SM_RESERVE = int(os.environ.get("ZP_RING_SM_RESERVE", "4"))
+RING_NCCL_CTAS = int(os.environ.get("ZP_RING_NCCL_CTAS", "2"))
 
 
 class RankContext:
@@ -50,6 +60,16 @@ class RankContext:
         self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.group = group
         self.comm_stream = torch.cuda.Stream(self.device) if world > 1 else None
+        # ring KV hops go through their own NCCL communicator capped at
+        # RING_NCCL_CTAS CTAs, so they fit in the SMs a ring round leaves free
+        # (RING_SM_RESERVE) and overlap the round instead of queueing behind it
+        self.ring_group = group
+        if world > 1 and dist.is_available() and dist.is_initialized() and RING_NCCL_CTAS > 0:
+            opts = dist.ProcessGroupNCCL.Options()
+            opts.config.max_ctas = RING_NCCL_CTAS
+            opts.config.min_ctas = 1
+            ranks = dist.get_process_group_ranks(group) if group is not None else list(range(world))
+            self.ring_group = dist.new_group(ranks=ranks, backend="nccl", pg_options=opts)
         self._ws: dict[str, torch.Tensor] = {}
         self.tracer = None  # trace.Tracer: measured timeline in the reference trace schema
 
@@ -184,13 +204,19 @@ def ring_p2p_ops(rp, round_index: int, cur: torch.Tensor, nxt: torch.Tensor, gro
     return ops_
 
 
+
+
 def _run_ring(ctx: RankContext, rp, dev_pack, dev_rounds, q, k, v, o, lse, scale):
     hkv, d = k.shape[1], k.shape[2]
     hq = q.shape[1]
     cs = torch.cuda.current_stream()
     xs = ctx.comm_stream
     rows = max(rp.held_rows)
-    bufs = [ctx.workspace(f"ringkv{j}", (rows, 2, hkv, d), torch.bfloat16) for j in (0, 1)]
+    # three KV buffers: the hop that fills round r+1's buffer waits only for
+    # round r-2 (its last reader), so KV sets travel around the ring at link
+    # speed instead of in lockstep with the slowest member's compute
+    nbuf = 3 if rp.group_size > 2 else 2
+    bufs = [ctx.workspace(f"ringkv{j}", (rows, 2, hkv, d), torch.bfloat16) for j in range(nbuf)]
     st_o = ctx.workspace("ring_state_o", (max(rp.state_rows, 1), hq, d), torch.float32)
     st_ml = ctx.workspace("ring_state_ml", (2, hq, max(rp.state_rows, 1)), torch.float32)
     n_pack = rp.pack_ranges.shape[0]
@@ -199,19 +225,20 @@ def _run_ring(ctx: RankContext, rp, dev_pack, dev_rounds, q, k, v, o, lse, scale
     ops.copy_rows(bufs[0][:, 1], v, dev_pack, n_pack, max_pack)
     ready = torch.cuda.Event()
     ready.record(cs)
-    done = None
+    done_at: dict[int, torch.cuda.Event] = {}
     g = rp.group_size
     for r in range(g):
-        cur, nxt = bufs[r % 2], bufs[(r + 1) % 2]
+        cur, nxt = bufs[r % nbuf], bufs[(r + 1) % nbuf]
         nxt_ready = None
         if r < g - 1:
             xs.wait_event(ready)
-            if done is not None:
-                xs.wait_event(done)  # round r-1 finished reading nxt
+            last_reader = r + 1 - nbuf  # the round that last read nxt
+            if last_reader >= 0:
+                xs.wait_event(done_at[last_reader])
             with torch.cuda.stream(xs), ctx.span("intra-comm", "kv.send",
                                                   {"ring": rp.ring_index, "round": r, "tokens": rp.send_rows(r),
                                                    "dst": rp.next_rank}, xs):
-                p2p = ring_p2p_ops(rp, r, cur, nxt, ctx.group)
+                p2p = ring_p2p_ops(rp, r, cur, nxt, ctx.ring_group)
                 if p2p:
                     for req in dist.batch_isend_irecv(p2p):
                         req.wait()
@@ -224,10 +251,14 @@ def _run_ring(ctx: RankContext, rp, dev_pack, dev_rounds, q, k, v, o, lse, scale
         with ctx.span("compute", "intra_node.attn",
                       {"ring": rp.ring_index, "round": r, "pairs": rp.rounds[r].work.pairs_per_head}):
             if work.n:
+                # while the next hop is in flight, leave SMs to its P2P kernels
+                prev = ops.set_sm_reserve(RING_SM_RESERVE if nxt_ready is not None else 0)
                 ops.attn_fwd(q, cur[:n_kv, 0], cur[:n_kv, 1], work.items, work.n, work.segs, o, lse,
                              st_o, st_ml, softmax_scale=scale)
+                ops.set_sm_reserve(prev)
         done = torch.cuda.Event()
         done.record(cs)
+        done_at[r] = done
         if nxt_ready is not None:
             ready = nxt_ready
     if xs is not None:
@@ -361,7 +392,7 @@ def _run_ring_backward(ctx: RankContext, rp, dev_pack, dev_rounds, dev_unpack, q
             with torch.cuda.stream(xs), ctx.span("intra-comm", "kv.send",
                                                   {"ring": rp.ring_index, "round": r, "tokens": rp.send_rows(r),
                                                    "dst": rp.next_rank}, xs):
-                p2p = ring_p2p_ops(rp, r, kv[cur], kv[nxt], ctx.group)
+                p2p = ring_p2p_ops(rp, r, kv[cur], kv[nxt], ctx.ring_group)
                 if p2p:
                     for req in dist.batch_isend_irecv(p2p):
                         req.wait()
@@ -394,11 +425,11 @@ def _run_ring_backward(ctx: RankContext, rp, dev_pack, dev_rounds, dev_unpack, q
                 zv[cur][:n_send].add_(av[cur][:n_send])
             p2p = []
             if n_send:
-                p2p += [dist.P2POp(dist.isend, zk[cur][:n_send], rp.next_rank, ctx.group),
-                        dist.P2POp(dist.isend, zv[cur][:n_send], rp.next_rank, ctx.group)]
+                p2p += [dist.P2POp(dist.isend, zk[cur][:n_send], rp.next_rank, ctx.ring_group),
+                        dist.P2POp(dist.isend, zv[cur][:n_send], rp.next_rank, ctx.ring_group)]
             if n_recv:
-                p2p += [dist.P2POp(dist.irecv, ak[nxt][:n_recv], rp.prev_rank, ctx.group),
-                        dist.P2POp(dist.irecv, av[nxt][:n_recv], rp.prev_rank, ctx.group)]
+                p2p += [dist.P2POp(dist.irecv, ak[nxt][:n_recv], rp.prev_rank, ctx.ring_group),
+                        dist.P2POp(dist.irecv, av[nxt][:n_recv], rp.prev_rank, ctx.ring_group)]
             if p2p:
                 for req in dist.batch_isend_irecv(p2p):
                     req.wait()

@@ -74,6 +74,12 @@ def upload_worklist(wl: WorkList, device: torch.device) -> tuple[torch.Tensor, t
     return items, segs
 
 
+def set_sm_reserve(sms: int) -> int:
+    """SMs the attention launches leave free (zp_attn_set_sm_reserve);
+    returns the previous value."""
+    return int(_native.lib().zp_attn_set_sm_reserve(int(sms)))
+
+
 def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, items: torch.Tensor, n_items: int,
              segs: torch.Tensor, o: torch.Tensor, lse: torch.Tensor,
              state_o: torch.Tensor | None = None, state_ml: torch.Tensor | None = None,
