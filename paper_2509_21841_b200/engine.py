@@ -60,9 +60,11 @@ class RankContext:
         self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.group = group
         self.comm_stream = torch.cuda.Stream(self.device) if world > 1 else None
-        # ring KV hops go through their own NCCL communicator capped at
+        # forward ring KV hops go through their own NCCL communicator capped at
         # RING_NCCL_CTAS CTAs, so they fit in the SMs a ring round leaves free
-        # (RING_SM_RESERVE) and overlap the round instead of queueing behind it
+        # (RING_SM_RESERVE) and overlap the round instead of queueing behind it;
+        # the backward's (non-persistent kernel, larger fp32 partials) stay on
+        # the uncapped group
         self.ring_group = group
         if world > 1 and dist.is_available() and dist.is_initialized() and RING_NCCL_CTAS > 0:
             opts = dist.ProcessGroupNCCL.Options()
@@ -392,7 +394,7 @@ def _run_ring_backward(ctx: RankContext, rp, dev_pack, dev_rounds, dev_unpack, q
             with torch.cuda.stream(xs), ctx.span("intra-comm", "kv.send",
                                                   {"ring": rp.ring_index, "round": r, "tokens": rp.send_rows(r),
                                                    "dst": rp.next_rank}, xs):
-                p2p = ring_p2p_ops(rp, r, kv[cur], kv[nxt], ctx.ring_group)
+                p2p = ring_p2p_ops(rp, r, kv[cur], kv[nxt], ctx.group)
                 if p2p:
                     for req in dist.batch_isend_irecv(p2p):
                         req.wait()
@@ -425,11 +427,11 @@ def _run_ring_backward(ctx: RankContext, rp, dev_pack, dev_rounds, dev_unpack, q
                 zv[cur][:n_send].add_(av[cur][:n_send])
             p2p = []
             if n_send:
-                p2p += [dist.P2POp(dist.isend, zk[cur][:n_send], rp.next_rank, ctx.ring_group),
-                        dist.P2POp(dist.isend, zv[cur][:n_send], rp.next_rank, ctx.ring_group)]
+                p2p += [dist.P2POp(dist.isend, zk[cur][:n_send], rp.next_rank, ctx.group),
+                        dist.P2POp(dist.isend, zv[cur][:n_send], rp.next_rank, ctx.group)]
             if n_recv:
-                p2p += [dist.P2POp(dist.irecv, ak[nxt][:n_recv], rp.prev_rank, ctx.ring_group),
-                        dist.P2POp(dist.irecv, av[nxt][:n_recv], rp.prev_rank, ctx.ring_group)]
+                p2p += [dist.P2POp(dist.irecv, ak[nxt][:n_recv], rp.prev_rank, ctx.group),
+                        dist.P2POp(dist.irecv, av[nxt][:n_recv], rp.prev_rank, ctx.group)]
             if p2p:
                 for req in dist.batch_isend_irecv(p2p):
                     req.wait()
