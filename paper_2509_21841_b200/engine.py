@@ -255,9 +255,11 @@ def _run_ring(ctx: RankContext, rp, dev_pack, dev_rounds, q, k, v, o, lse, scale
             if work.n:
                 # while the next hop is in flight, leave SMs to its P2P kernels
                 prev = ops.set_sm_reserve(RING_SM_RESERVE if nxt_ready is not None else 0)
-                ops.attn_fwd(q, cur[:n_kv, 0], cur[:n_kv, 1], work.items, work.n, work.segs, o, lse,
-                             st_o, st_ml, softmax_scale=scale)
-                ops.set_sm_reserve(prev)
+                try:
+                    ops.attn_fwd(q, cur[:n_kv, 0], cur[:n_kv, 1], work.items, work.n, work.segs, o, lse,
+                                 st_o, st_ml, softmax_scale=scale)
+                finally:
+                    ops.set_sm_reserve(prev)
         done = torch.cuda.Event()
         done.record(cs)
         done_at[r] = done
