@@ -151,3 +151,19 @@ print("NO ERROR")
 '''
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert "NO ERROR" not in r.stdout and r.returncode != 0, r.stdout + r.stderr
+
+
+def test_sm_reserve_leaves_results_bit_identical():
+    """zp_attn_set_sm_reserve (SMs left free for ring-hop kernels) only caps the
+    persistent grid: the output is bit-identical, and the previous value comes back."""
+    seqlens = [3000, 700, 129]
+    q, k, v = make_qkv(sum(seqlens), seed=11)
+    o_full, lse_full = ops.varlen_attention(q, k, v, seqlens)
+    prev = ops.set_sm_reserve(140)  # leaves only a few CTA pairs running
+    try:
+        o_cap, lse_cap = ops.varlen_attention(q, k, v, seqlens)
+    finally:
+        assert ops.set_sm_reserve(prev) == 140
+    torch.cuda.synchronize()
+    assert torch.equal(o_full, o_cap)
+    assert torch.equal(lse_full, lse_cap)
