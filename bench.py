@@ -455,6 +455,11 @@ def cpu_baseline(plan, sched, seconds: float):
     done_pairs, spent, rows = 0, 0.0, 0
     block = 256
     while spent < seconds and rows < n:
+        if done_pairs:
+            # size the next block to the remaining budget (blocks double otherwise)
+            rate = spent / done_pairs
+            while block > 64 and rate * block * (rows + block / 2) > max(seconds - spent, 0.25 * seconds):
+                block //= 2
         r1 = min(n, rows + block)
         q = rng.standard_normal((r1 - rows, hq, d), dtype=np.float32)
         t0 = time.perf_counter()
@@ -485,7 +490,7 @@ def run_reference(args):
     name, batch, cluster = workload(args.gpus)
     plan = P.build_plan(batch, cluster)
     sched = S.build_schedule(plan)
-    per_step = max(5.0, min(30.0, 150.0 / max(1, args.steps + args.warmup)))
+    per_step = max(3.0, min(30.0, 100.0 / max(1, args.steps + args.warmup)))
     vals = []
     for i in range(args.warmup + args.steps):
         cb = cpu_baseline(plan, sched, per_step)
