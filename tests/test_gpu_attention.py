@@ -167,3 +167,20 @@ def test_sm_reserve_leaves_results_bit_identical():
     torch.cuda.synchronize()
     assert torch.equal(o_full, o_cap)
     assert torch.equal(lse_full, lse_cap)
+
+
+def test_single_cta_kernel_gqa_group_of_two():
+    """A GQA group of 2 (16 query / 8 KV heads) cannot pair head pairs of one
+    KV head across a CTA pair, so it runs the single-CTA (cta_group::1) kernel."""
+    seqlens = [1000, 130, 2049]
+    t = sum(seqlens)
+    q, k, v = make_qkv(t, hq=16, hkv=8, seed=21)
+    o, lse = ops.varlen_attention(q, k, v, seqlens)
+    torch.cuda.synchronize()
+    r = 0
+    for n in seqlens:
+        pos = torch.arange(n, device="cuda")
+        ro, rl = ref_attention(q[r:r + n], k[r:r + n], v[r:r + n], pos, pos)
+        assert (o[r:r + n].float() - ro).abs().max().item() <= MAX_ABS
+        assert (lse[:, r:r + n] - rl).abs().max().item() <= 1e-2
+        r += n
