@@ -122,6 +122,17 @@ struct StepCursor {
 
 #ifdef ZP_TRACE
 __device__ unsigned long long g_zp_btrace[4096];
+// per item (CTA): globaltimer at entry / K,V landed / exit, and the step count
+__device__ unsigned long long g_zp_bitems[16384 * 4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+  return t;
+}
+#define ZP_BITEM(e, v)                                                    \
+  do {                                                                    \
+    if (blockIdx.x < 16384) g_zp_bitems[blockIdx.x * 4 + (e)] = (v);      \
+  } while (0)
 #define ZP_BSTAMP(slot)                                                  \
   do {                                                                   \
     if (blockIdx.x == 0 && (slot) >= 0 && (slot) < 4096) {               \
@@ -181,6 +192,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const zp_bwd_item it = args.items[blockIdx.x];
+#ifdef ZP_TRACE
+  if (threadIdx.x == 0) ZP_BITEM(0, gtimer());
+#endif
   const int kvh = it.kv_head;
 
   if (threadIdx.x == 0) {
@@ -258,6 +272,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mbar_wait(bar(B_KV), 0);
       tc_fence_after();
+#ifdef ZP_TRACE
+      if (lane == 0) {
+        ZP_BITEM(1, gtimer());
+        ZP_BITEM(3, (unsigned long long)n_steps);
+      }
+#endif
       auto issue_sdp = [&](int m) {
         const int buf = m & 1, qs = m % kQStages;
         if (lane == 0 && m < 256) ZP_BSTAMP(3072 + m * 4 + 0);
@@ -471,6 +491,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+#ifdef ZP_TRACE
+  if (threadIdx.x == 0) ZP_BITEM(2, gtimer());
+#endif
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
@@ -504,6 +527,10 @@ __global__ void bwd_delta_kernel(const __nv_bfloat16* __restrict__ o, const __nv
 #include "zp_host.h"
 
 #ifdef ZP_TRACE
+extern "C" ZP_API int zp_debug_bitems(unsigned long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, zp::bwd::g_zp_bitems, sizeof(unsigned long long) * (n < 65536 ? n : 65536)) ==
+                 cudaSuccess ? 0 : -1;
+}
 extern "C" ZP_API int zp_debug_btrace(unsigned long long* host, int n) {
   return cudaMemcpyFromSymbol(host, zp::bwd::g_zp_btrace, sizeof(unsigned long long) * (n < 4096 ? n : 4096)) ==
                  cudaSuccess ? 0 : -1;
