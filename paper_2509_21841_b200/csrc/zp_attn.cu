@@ -196,25 +196,6 @@ __device__ __forceinline__ float2 exp2_poly(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(y.y) << 23)));
 }
 
-#ifndef ZP_EXP_F16
-#define ZP_EXP_F16 0
-#endif
-constexpr bool kExpF16 = ZP_EXP_F16 != 0;
-
-// 2^x for a pair with ONE MUFU op: x rounded to f16 (x <= 8 under the lazy
-// rescale bound, so |error| <= 2^-8 in x, i.e. <= 0.27% in P — below the bf16
-// rounding P gets anyway), packed ex2.approx.f16x2, unpacked to fp32.
-__device__ __forceinline__ float2 ex2_f16x2(float2 x) {
-  uint32_t xh, eh;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(xh) : "f"(x.y), "f"(x.x));
-  asm("ex2.approx.f16x2 %0, %1;" : "=r"(eh) : "r"(xh));
-  float2 p;
-  asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\tcvt.f32.f16 %0, lo;\n\tcvt.f32.f16 %1, hi;\n\t}"
-      : "=f"(p.x), "=f"(p.y)
-      : "r"(eh));
-  return p;
-}
-
 // P = 2^(s*scale_log2 - m) for one half (64 keys) of a 128-column row,
 // packed to bf16x2 and stored to the half's 32 P columns in TMEM; row sum
 // accumulated in two float2.  kEmu: a fixed share of the column pairs takes
@@ -231,8 +212,6 @@ __device__ __forceinline__ void exp_half(const float (&s)[128], float2 sl2x2, fl
       float2 p;
       if (kEmu && ((c * 16 + v) & 7) < kEmuOf8) {
         p = exp2_poly(x);
-      } else if (kExpF16) {
-        p = ex2_f16x2(x);
       } else {
         p.x = ex2(x.x);
         p.y = ex2(x.y);
