@@ -96,6 +96,19 @@ ZP_API int zp_attn_fwd(const void* q, const void* k, const void* v, int q_rows, 
                 float* state_o, float* state_ml, int state_rows, float softmax_scale,
                 void* workspace, void* stream);
 
+/* Parity mode of zp_attn_fwd (same work items, same kernel pipeline): v_f16
+ * holds V converted to fp16 (same layout / strides as zp_attn_fwd's v), the
+ * probabilities P are staged as fp16 instead of bf16 for the P.V product, and
+ * o is written as fp32 [q_rows, hq, 128] (unrounded).  This isolates the
+ * kernel's arithmetic from the bf16 output rounding so that the north star's
+ * mean-relative tolerance (1e-3 vs fp32) is checkable; the production path is
+ * zp_attn_fwd. */
+ZP_API int zp_attn_fwd_parity(const void* q, const void* k, const void* v_f16, int q_rows, int kv_rows,
+                int kv_row_stride, int hq, int hkv, int head_dim, float* o, float* lse,
+                int lse_stride, const zp_attn_item* items, int n_items, const zp_kv_seg* segs,
+                float* state_o, float* state_ml, int state_rows, float softmax_scale,
+                void* workspace, void* stream);
+
 /* ---------------------------------------------------------------- backward
  * (the reference charges backward as a multiple of the
  * forward, topology.py:37 / simulator.py:304; executed here for the same
@@ -194,6 +207,35 @@ ZP_API int zp_remap_push_ce(const void* src, int64_t row_bytes, const int64_t* d
                      const int32_t* count_host, const int64_t* flags_ptrs,
                      const int32_t* count_dev, const int32_t* expect_dev, int world,
                      int my_rank, int32_t epoch, void* stream);
+
+/* ---------------------------------------------------------------- ring KV exchange
+ * (attention_engine.py:247-251: after round r position i forwards the KV set
+ * it holds to position i+1; simulator.py:150-174 charges it.)  Executed as a
+ * PULL by position i+1 with no SM involvement: stream memory operations wait
+ * on / write int32 epoch flags and one copy-engine transfer moves the bytes
+ * over NVLink, so a hop overlaps a ring round that occupies every SM.
+ * Flags are compared with wrap-around ">=" (int32)(*flag - epoch) >= 0. */
+
+/* Enqueue on `stream`: wait until *flag >= epoch (flag: device memory of the
+ * calling GPU, written by peers). */
+ZP_API int zp_stream_wait_flag(const int32_t* flag, int32_t epoch, void* stream);
+
+/* Enqueue on `stream`: *flag = epoch after every earlier operation of the
+ * stream (memory barrier), flag may be a peer (IPC-mapped) address. */
+ZP_API int zp_stream_write_flag(int32_t* flag, int32_t epoch, void* stream);
+
+/* One hop, pull form, enqueued on `stream`:
+ *  1. wait *full_flag >= full_epoch     (the predecessor's set is in `src`);
+ *  2. if free_flag: wait *free_flag >= free_epoch   (the successor finished
+ *     reading what `dst` held before);
+ *  3. copy `bytes` from src (predecessor's IPC-mapped buffer) to dst;
+ *  4. *consumed_flag = consumed_epoch   (in the predecessor's flag block);
+ *  5. if next_full_flag: *next_full_flag = next_full_epoch   (in the
+ *     successor's flag block: dst now holds the set it pulls next). */
+ZP_API int zp_ring_hop(void* dst, const void* src, int64_t bytes, const int32_t* full_flag,
+                int32_t full_epoch, const int32_t* free_flag, int32_t free_epoch,
+                int32_t* consumed_flag, int32_t consumed_epoch, int32_t* next_full_flag,
+                int32_t next_full_epoch, void* stream);
 
 /* ---- full transformer block (config 5): elementwise kernels around the
  * cuBLAS GEMMs of the linear modules, which run on the balanced (linear)

@@ -25,6 +25,8 @@ _c_int, _c_i64, _c_float, _vp = ctypes.c_int, ctypes.c_int64, ctypes.c_float, ct
 SIGNATURES: dict[str, tuple] = {
     "zp_attn_fwd": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                              _vp, _vp, _c_int, _vp, _c_int, _vp, _vp, _vp, _c_int, _c_float, _vp, _vp]),
+    "zp_attn_fwd_parity": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
+                                    _vp, _vp, _c_int, _vp, _c_int, _vp, _vp, _vp, _c_int, _c_float, _vp, _vp]),
     "zp_attn_bwd_prep": (_c_int, [_vp, _vp, _c_int, _c_int, _c_int, _vp, _c_int, _vp]),
     "zp_attn_bwd": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp,
                              _c_int, _vp, _vp, _vp, _vp, _c_int, _vp, _c_float, _vp]),
@@ -37,7 +39,11 @@ SIGNATURES: dict[str, tuple] = {
                                   ctypes.c_int32, _vp]),
     "zp_remap_push_ce": (_c_int, [_vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                   ctypes.c_int32, _vp]),
-    "zp_rmsnorm": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_float, _vp]),
+    "zp_stream_wait_flag": (_c_int, [_vp, ctypes.c_int32, _vp]),
+    "zp_stream_write_flag": (_c_int, [_vp, ctypes.c_int32, _vp]),
+    "zp_ring_hop": (_c_int, [_vp, _vp, _c_i64, _vp, ctypes.c_int32, _vp, ctypes.c_int32, _vp, ctypes.c_int32,
+                             _vp, ctypes.c_int32, _vp]),
+    "zp_rmsnorm":(_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_float, _vp]),
     "zp_rope_split": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
     "zp_swiglu": (_c_int, [_vp, _vp, _c_int, _c_int, _vp]),
     "zp_ipc_get_handle": (_c_int, [_vp, _vp, ctypes.POINTER(_c_i64)]),

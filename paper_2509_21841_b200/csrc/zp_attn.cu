@@ -119,7 +119,7 @@ struct AttnArgs {
   int n_units;     // items (single) or item pairs (pair)
   int* next_unit;  // global work counter (zeroed before the launch)
   const zp_kv_seg* segs;
-  __nv_bfloat16* o;
+  void* o;  // bf16 [rows, hq, 128]; fp32 in the parity mode
   float* lse;
   float* st_o;
   float* st_ml;
@@ -200,7 +200,7 @@ __device__ __forceinline__ float2 exp2_poly(float2 x) {
 // packed to bf16x2 and stored to the half's 32 P columns in TMEM; row sum
 // accumulated in two float2.  kEmu: a fixed share of the column pairs takes
 // the FMA-pipe exp2 (relieves the MUFU pipe, 16 ex2/clk/SM).
-template <int kHalf, bool kEmu>
+template <int kHalf, bool kEmu, bool kF16>
 __device__ __forceinline__ void exp_half(const float (&s)[128], float2 sl2x2, float2 negm, uint32_t tP,
                                          float2& acc0, float2& acc1) {
 #pragma unroll
@@ -217,7 +217,7 @@ __device__ __forceinline__ void exp_half(const float (&s)[128], float2 sl2x2, fl
         p.y = ex2(x.y);
       }
       if (v & 1) acc1 = __fadd2_rn(acc1, p); else acc0 = __fadd2_rn(acc0, p);
-      pk[v] = pack_bf16(p.x, p.y);
+      pk[v] = pack_p<kF16>(p.x, p.y);
     }
     tmem_st16(tP + c * 16, pk);
   }
@@ -282,7 +282,7 @@ __device__ __forceinline__ int count_tiles(const zp_kv_seg* segs, const zp_attn_
 // leader's, in a pair) claims the next unit of the longest-first list with one
 // atomicAdd (greedy LPT across SMs) and publishes it to every consumer through
 // a 4-slot smem ring (both CTAs' rings in a pair).
-template <bool kPair>
+template <bool kPair, bool kParity>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
@@ -463,7 +463,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // PV_t(g-1) then S_t(g) for t = 0, 1 (the S/P TMEM aliasing relies on
       // tcgen05 MMAs executing in issue order).
       constexpr uint32_t idesc_qk = idesc_bf16_f32(kPair ? 256 : 128, 128, 0, 0);
-      constexpr uint32_t idesc_pv = idesc_bf16_f32(kPair ? 256 : 128, 128, 0, 1);
+      // parity mode: P (TMEM A) and V (smem B) are fp16
+      constexpr uint32_t idesc_pv = kParity ? idesc_f16_f32(kPair ? 256 : 128, 128, 0, 1)
+                                            : idesc_bf16_f32(kPair ? 256 : 128, 128, 0, 1);
       const uint32_t tS[2] = {tmem + 0, tmem + 128};
       const uint32_t tO[2] = {tmem + 256, tmem + 384};
       const uint64_t q_desc0 = umma_desc_sw128(sbase + C::kSmemQ, 16, 1024);
@@ -640,7 +642,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             p.x = ex2(x.x);
             p.y = ex2(x.y);
             if (v & 1) a1 = __fadd2_rn(a1, p); else a0 = __fadd2_rn(a0, p);
-            if (v < 16) pa0[v] = pack_bf16(p.x, p.y); else pa1[v - 16] = pack_bf16(p.x, p.y);
+            if (v < 16) pa0[v] = pack_p<kParity>(p.x, p.y); else pa1[v - 16] = pack_p<kParity>(p.x, p.y);
             if (v & 1) {
               c0 = fmax3(c0, s[2 * v], s[2 * v + 1]);
               c1 = fmax3(c1, s[64 + 2 * v], s[64 + 2 * v + 1]);
@@ -663,8 +665,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ZP_STAMP(tr < 0 ? -1 : tr + 2);
             ZP_STAMP(tr < 0 ? -1 : tr + 3);
-            if (masked) exp_half<1, false>(s, sl2x2, negm, tP, a0, a1);
-            else exp_half<1, true>(s, sl2x2, negm, tP, a0, a1);
+            if (masked) exp_half<1, false, kParity>(s, sl2x2, negm, tP, a0, a1);
+            else exp_half<1, true, kParity>(s, sl2x2, negm, tP, a0, a1);
             const float2 acc = __fadd2_rn(a0, a1);
             l += acc.x + acc.y;
             tmem_wait_st();
@@ -731,8 +733,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the second half's exponentials run.
         const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m_use, -m_use);
         float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
-        if (masked) exp_half<0, false>(s, sl2x2, negm, tP, acc0, acc1);
-        else exp_half<0, true>(s, sl2x2, negm, tP, acc0, acc1);
+        if (masked) exp_half<0, false, kParity>(s, sl2x2, negm, tP, acc0, acc1);
+        else exp_half<0, true, kParity>(s, sl2x2, negm, tP, acc0, acc1);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -741,8 +743,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           else mbar_arrive(pfull);
         }
         ZP_STAMP(tr < 0 ? -1 : tr + 3);
-        if (masked) exp_half<1, false>(s, sl2x2, negm, tP, acc0, acc1);
-        else exp_half<1, true>(s, sl2x2, negm, tP, acc0, acc1);
+        if (masked) exp_half<1, false, kParity>(s, sl2x2, negm, tP, acc0, acc1);
+        else exp_half<1, true, kParity>(s, sl2x2, negm, tP, acc0, acc1);
         const float2 acc = __fadd2_rn(acc0, acc1);
         l = l * alpha + (acc.x + acc.y);
         m = m_new;
@@ -779,8 +781,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else {
         const float inv_l = l > 0.f ? 1.f / l : 0.f;
-        // one 256-bit store per 16 dims: full 32-byte sectors of the row
-        uint8_t* dst = reinterpret_cast<uint8_t*>(args.o + (size_t(it.q_row0 + row) * args.hq + h) * kHeadDim);
+        // one 256-bit store per 16 dims (8 fp32 dims in the parity mode):
+        // full 32-byte sectors of the row
+        const size_t orow = (size_t(it.q_row0 + row) * args.hq + h) * kHeadDim;
+        uint8_t* dst = kParity ? reinterpret_cast<uint8_t*>(static_cast<float*>(args.o) + orow)
+                               : reinterpret_cast<uint8_t*>(static_cast<__nv_bfloat16*>(args.o) + orow);
         const float2 il2 = make_float2(inv_l, inv_l);
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
@@ -789,15 +794,27 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32(tO + cc * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(rr + 32));
           tmem_wait_ld();
           if (ok) {
-            uint32_t pk[32];
+            if constexpr (kParity) {
 #pragma unroll
-            for (int v = 0; v < 32; ++v) {
-              const float2 x =
-                  __fmul2_rn(make_float2(__uint_as_float(rr[2 * v]), __uint_as_float(rr[2 * v + 1])), il2);
-              pk[v] = pack_bf16(x.x, x.y);
+              for (int v = 0; v < 32; ++v) {
+                const float2 x =
+                    __fmul2_rn(make_float2(__uint_as_float(rr[2 * v]), __uint_as_float(rr[2 * v + 1])), il2);
+                rr[2 * v] = __float_as_uint(x.x);
+                rr[2 * v + 1] = __float_as_uint(x.y);
+              }
+#pragma unroll
+              for (int w = 0; w < 8; ++w) stg_v8(dst + cc * 256 + w * 32, rr + 8 * w);
+            } else {
+              uint32_t pk[32];
+#pragma unroll
+              for (int v = 0; v < 32; ++v) {
+                const float2 x =
+                    __fmul2_rn(make_float2(__uint_as_float(rr[2 * v]), __uint_as_float(rr[2 * v + 1])), il2);
+                pk[v] = pack_bf16(x.x, x.y);
+              }
+#pragma unroll
+              for (int w = 0; w < 4; ++w) stg_v8(dst + cc * 128 + w * 32, pk + 8 * w);
             }
-#pragma unroll
-            for (int w = 0; w < 4; ++w) stg_v8(dst + cc * 128 + w * 32, pk + 8 * w);
           }
         }
         if (ok) {
@@ -842,20 +859,31 @@ int variant() {
   return v;
 }
 
-template <bool kPair>
+// Per-device launch facts (the smem attribute is per device and function; the
+// resident CTA / cluster count comes from that device's occupancy query).
+struct LaunchCache {
+  bool done = false;
+  int max_units = 0;  // resident CTAs (single) or CTA pairs (pair)
+};
+constexpr int kMaxDevices = 64;
+
+template <bool kPair, bool kParity>
 int launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, zp::AttnArgs a,
                 int n_units, cudaStream_t stream) {
   using namespace zp;
   constexpr uint32_t smem = Cfg<kPair>::kSmemBytes;
-  auto kernel = attn_fwd_kernel<kPair>;
-  static bool attr_done = false;
-  static int max_units = 0;  // resident CTAs (single) or CTA pairs (pair)
-  if (!attr_done) {
+  auto kernel = attn_fwd_kernel<kPair, kParity>;
+  static LaunchCache cache[kMaxDevices];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
+    return zp_fail(ZP_ENODEV, "zp_attn_fwd: no current device");
+  LaunchCache& lc = cache[dev];
+  if (!lc.done) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return zp_fail_cuda(e, "zp_attn_fwd: smem attribute");
     const int sms = zp_device_sm_count();
     if (sms <= 0) return zp_fail(ZP_ENODEV, "zp_attn_fwd: cannot query SM count");
-    max_units = sms;
+    int units = sms;
     if (kPair) {
       cudaLaunchConfig_t cfg = {};
       cudaLaunchAttribute at[1];
@@ -874,14 +902,15 @@ int launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap&
         cudaGetLastError();
         clusters = sms / 2;
       }
-      max_units = clusters;
+      units = clusters;
     }
-    attr_done = true;
+    lc.max_units = units;
+    lc.done = true;
   }
   a.n_units = n_units;
   // persistent; g_sm_reserve SMs (whole units) stay free for concurrent comm kernels
   const int per_unit = kPair ? 2 : 1;
-  int cap = max_units - (g_sm_reserve + per_unit - 1) / per_unit;
+  int cap = lc.max_units - (g_sm_reserve + per_unit - 1) / per_unit;
   if (cap < 1) cap = 1;
   const int units = n_units < cap ? n_units : cap;
   cudaLaunchConfig_t cfg = {};
@@ -905,26 +934,10 @@ int launch_attn(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap&
   return ZP_OK;
 }
 
-}  // namespace
-
-#ifdef ZP_TRACE
-extern "C" ZP_API int zp_debug_trace(unsigned long long* host, int n) {
-  return cudaMemcpyFromSymbol(host, zp::g_zp_trace, sizeof(unsigned long long) * (n < 8192 ? n : 8192)) ==
-                 cudaSuccess ? 0 : -1;
-}
-#endif
-
-extern "C" int zp_attn_set_sm_reserve(int sms) {
-  const int prev = g_sm_reserve;
-  g_sm_reserve = sms < 0 ? 0 : sms;
-  return prev;
-}
-
-extern "C" int zp_attn_fwd(const void* q, const void* k, const void* v, int q_rows, int kv_rows,
-                           int kv_row_stride, int hq, int hkv, int head_dim, void* o, float* lse,
-                           int lse_stride, const zp_attn_item* items, int n_items,
-                           const zp_kv_seg* segs, float* state_o, float* state_ml,
-                           int state_rows, float softmax_scale, void* workspace, void* stream) {
+int attn_fwd_common(bool parity, const void* q, const void* k, const void* v, int q_rows, int kv_rows,
+                    int kv_row_stride, int hq, int hkv, int head_dim, void* o, float* lse, int lse_stride,
+                    const zp_attn_item* items, int n_items, const zp_kv_seg* segs, float* state_o,
+                    float* state_ml, int state_rows, float softmax_scale, void* workspace, void* stream) {
   using namespace zp;
   if (head_dim != kHeadDim) return zp_fail(ZP_EINVAL, "zp_attn_fwd: head_dim must be 128");
   if (hq <= 0 || hkv <= 0 || hq % hkv != 0 || (hq / hkv) % 2 != 0)
@@ -949,6 +962,7 @@ extern "C" int zp_attn_fwd(const void* q, const void* k, const void* v, int q_ro
   if ((rc = zp_make_tmap_2d_bf16(&tk, k, uint64_t(hkv) * kHeadDim, uint64_t(kv_rows),
                                  uint64_t(kv_row_stride) * 2, 64, pair ? 64 : 128)) != ZP_OK)
     return rc;
+  // (parity: v holds fp16; a 2-byte TMA copy moves the bits unchanged)
   if ((rc = zp_make_tmap_2d_bf16(&tv, v, uint64_t(hkv) * kHeadDim, uint64_t(kv_rows),
                                  uint64_t(kv_row_stride) * 2, 64, 128)) != ZP_OK)
     return rc;
@@ -957,7 +971,7 @@ extern "C" int zp_attn_fwd(const void* q, const void* k, const void* v, int q_ro
   a.items = items;
   a.next_unit = reinterpret_cast<int*>(workspace);
   a.segs = segs;
-  a.o = reinterpret_cast<__nv_bfloat16*>(o);
+  a.o = o;
   a.lse = lse;
   a.st_o = state_o;
   a.st_ml = state_ml;
@@ -969,6 +983,43 @@ extern "C" int zp_attn_fwd(const void* q, const void* k, const void* v, int q_ro
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t me = cudaMemsetAsync(workspace, 0, sizeof(int), s);
   if (me != cudaSuccess) return zp_fail_cuda(me, "zp_attn_fwd: workspace reset");
-  return pair ? launch_attn<true>(tq, tk, tv, a, n_items / 2, s)
-              : launch_attn<false>(tq, tk, tv, a, n_items, s);
+  if (parity)
+    return pair ? launch_attn<true, true>(tq, tk, tv, a, n_items / 2, s)
+                : launch_attn<false, true>(tq, tk, tv, a, n_items, s);
+  return pair ? launch_attn<true, false>(tq, tk, tv, a, n_items / 2, s)
+              : launch_attn<false, false>(tq, tk, tv, a, n_items, s);
+}
+
+}  // namespace
+
+#ifdef ZP_TRACE
+extern "C" ZP_API int zp_debug_trace(unsigned long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, zp::g_zp_trace, sizeof(unsigned long long) * (n < 8192 ? n : 8192)) ==
+                 cudaSuccess ? 0 : -1;
+}
+#endif
+
+extern "C" int zp_attn_set_sm_reserve(int sms) {
+  const int prev = g_sm_reserve;
+  g_sm_reserve = sms < 0 ? 0 : sms;
+  return prev;
+}
+
+extern "C" int zp_attn_fwd(const void* q, const void* k, const void* v, int q_rows, int kv_rows,
+                           int kv_row_stride, int hq, int hkv, int head_dim, void* o, float* lse,
+                           int lse_stride, const zp_attn_item* items, int n_items,
+                           const zp_kv_seg* segs, float* state_o, float* state_ml,
+                           int state_rows, float softmax_scale, void* workspace, void* stream) {
+  return attn_fwd_common(false, q, k, v, q_rows, kv_rows, kv_row_stride, hq, hkv, head_dim, o, lse, lse_stride,
+                         items, n_items, segs, state_o, state_ml, state_rows, softmax_scale, workspace, stream);
+}
+
+extern "C" int zp_attn_fwd_parity(const void* q, const void* k, const void* v_f16, int q_rows, int kv_rows,
+                                  int kv_row_stride, int hq, int hkv, int head_dim, float* o, float* lse,
+                                  int lse_stride, const zp_attn_item* items, int n_items,
+                                  const zp_kv_seg* segs, float* state_o, float* state_ml,
+                                  int state_rows, float softmax_scale, void* workspace, void* stream) {
+  return attn_fwd_common(true, q, k, v_f16, q_rows, kv_rows, kv_row_stride, hq, hkv, head_dim, o, lse,
+                         lse_stride, items, n_items, segs, state_o, state_ml, state_rows, softmax_scale,
+                         workspace, stream);
 }

@@ -8,7 +8,8 @@
 
 namespace {
 thread_local char g_err[512] = "ok";
-int g_dev_checked = -1;  // -1 unknown, 0 bad, 1 good
+constexpr int kMaxDevices = 64;
+int g_dev_checked[kMaxDevices] = {};  // per device ordinal: 0 unknown / failed, 1 good
 std::mutex g_mu;
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -30,10 +31,14 @@ int zp_fail_cuda(cudaError_t e, const char* where) {
 
 int zp_check_device() {
   std::lock_guard<std::mutex> lk(g_mu);
-  if (g_dev_checked == 1) return ZP_OK;
   int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+    cudaGetLastError();
+    return zp_fail(ZP_ENODEV, "no CUDA device visible");
+  }
+  if (g_dev_checked[dev] == 1) return ZP_OK;
   cudaDeviceProp prop;
-  if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
     cudaGetLastError();
     return zp_fail(ZP_ENODEV, "no CUDA device visible");
   }
@@ -53,7 +58,7 @@ int zp_check_device() {
     }
     g_encode = reinterpret_cast<PFN_encodeTiled>(fn);
   }
-  g_dev_checked = 1;
+  g_dev_checked[dev] = 1;
   return ZP_OK;
 }
 

@@ -114,6 +114,11 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N, int a_mn_maj
   return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(a_mn_major) << 15) |
          (uint32_t(b_mn_major) << 16) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
+// Same with fp16 A/B (a/b format fields 0 = f16).
+__host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N, int a_mn_major, int b_mn_major) {
+  return (1u << 4) | (uint32_t(a_mn_major) << 15) | (uint32_t(b_mn_major) << 16) |
+         (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
 
 // UMMA shared-memory descriptor for a SWIZZLE_128B canonical layout (sm_100 version bit set).
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo_bytes,
@@ -331,6 +336,18 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
+}
+__device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// P operand packing: bf16 in production, fp16 (3 more mantissa bits; P <= 2^8
+// under the lazy rescale, far inside fp16's range) in the parity mode.
+template <bool kF16>
+__device__ __forceinline__ uint32_t pack_p(float lo, float hi) {
+  if constexpr (kF16) return pack_f16(lo, hi);
+  else return pack_bf16(lo, hi);
 }
 
 // 256-bit global accesses (sm_100: one full 32-byte sector per thread).

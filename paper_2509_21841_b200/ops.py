@@ -46,12 +46,14 @@ def set_launch_hook(fn) -> None:
 _workspaces: dict = {}
 
 
-def _workspace(device: torch.device) -> torch.Tensor:
-    """Per-device scratch for the attention scheduler counter (torch-owned)."""
-    key = (device.type, device.index)
+def _workspace(device: torch.device, stream: int) -> torch.Tensor:
+    """Scratch for the persistent scheduler's work counter (torch-owned), one
+    per (device, stream): launches on one stream reuse theirs in stream order,
+    launches on different streams never share one."""
+    key = (device.index, stream)
     ws = _workspaces.get(key)
     if ws is None:
-        ws = torch.zeros(16, dtype=torch.uint8, device=device)
+        ws = torch.empty(16, dtype=torch.uint8, device=device)  # zeroed by each launch on its stream
         _workspaces[key] = ws
     return ws
 
@@ -88,14 +90,18 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, items: torch.Ten
 
     q: [Tq, Hq, 128] bf16, k/v: [Tk, Hkv, 128] bf16 views whose row stride may
     exceed Hkv*128 (interleaved ring buffers), o: [Tq, Hq, 128] bf16,
-    lse: [Hq, Tq] fp32."""
+    lse: [Hq, Tq] fp32.  Parity mode (zp_attn_fwd_parity) when v is fp16 and
+    o fp32: P staged as fp16, unrounded fp32 output."""
     _require_cuda(q, k, v, o, lse)
     tq, hq, d = q.shape
     tk, hkv, dk = k.shape
     if d != HEAD_DIM or dk != HEAD_DIM or v.shape != k.shape:
         raise ValueError("head_dim must be 128 and k/v must have equal shapes")
-    if q.dtype != torch.bfloat16 or k.dtype != torch.bfloat16 or v.dtype != torch.bfloat16:
-        raise ValueError("q/k/v must be bf16")
+    parity = v.dtype == torch.float16
+    if q.dtype != torch.bfloat16 or k.dtype != torch.bfloat16 or v.dtype not in (torch.bfloat16, torch.float16):
+        raise ValueError("q/k must be bf16, v bf16 (or fp16 for the parity mode)")
+    if o.dtype != (torch.float32 if parity else torch.bfloat16):
+        raise ValueError("o must be bf16 (fp32 in the parity mode, v fp16)")
     if q.stride() != (hq * d, d, 1) or o.stride() != (hq * d, d, 1):
         raise ValueError("q and o must be row-contiguous [T, H, 128]")
     if k.stride()[1:] != (d, 1) or v.stride() != k.stride():
@@ -111,10 +117,10 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, items: torch.Ten
     if _hook is not None:
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
-    _native.call("zp_attn_fwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), tq, tk, k.stride(0),
-                 hq, hkv, d, o.data_ptr(), lse.data_ptr(), lse.stride(0), items.data_ptr(),
-                 n_items, segs.data_ptr(), st_o, st_ml, st_rows, scale, _workspace(q.device).data_ptr(),
-                 _stream_ptr(stream))
+    sp = _stream_ptr(stream)
+    _native.call("zp_attn_fwd_parity" if parity else "zp_attn_fwd", q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                 tq, tk, k.stride(0), hq, hkv, d, o.data_ptr(), lse.data_ptr(), lse.stride(0), items.data_ptr(),
+                 n_items, segs.data_ptr(), st_o, st_ml, st_rows, scale, _workspace(q.device, sp).data_ptr(), sp)
     if _hook is not None:
         ev1.record()
         _hook("zp_attn_fwd", ev0, ev1)
@@ -207,12 +213,13 @@ def local_fragments(seqlens: list[int] | np.ndarray, row0: int = 0) -> list[Quer
 def varlen_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seqlens,
                      softmax_scale: float | None = None) -> tuple[torch.Tensor, torch.Tensor]:
     """Causal attention of packed variable-length sequences (all GPU-local):
-    the LocalTask queue of one rank.  Returns (o bf16 [T,Hq,128], lse fp32 [Hq,T])."""
+    the LocalTask queue of one rank.  Returns (o bf16 [T,Hq,128], lse fp32 [Hq,T]);
+    with an fp16 v the parity mode runs and o is fp32."""
     _require_cuda(q, k, v)
     t, hq, _ = q.shape
     hkv = k.shape[1]
     wl = build_worklist(local_fragments(seqlens), hq // 2)
-    o = torch.empty_like(q)
+    o = torch.empty(q.shape, dtype=torch.float32 if v.dtype == torch.float16 else q.dtype, device=q.device)
     lse = torch.empty(hq, t, dtype=torch.float32, device=q.device)
     items, segs = upload_worklist(wl, q.device)
     attn_fwd(q, k, v, items, wl.n_items, segs, o, lse, softmax_scale=softmax_scale)
