@@ -187,6 +187,25 @@ ZP_API int zp_remap_pull(void* dst, int64_t row_bytes, const int64_t* src_ptrs,
                   const int64_t* flags_ptrs, const int32_t* readers, int world, int my_rank,
                   int32_t epoch, int max_count, void* stream);
 
+/* zp_remap_push / zp_remap_pull with a subset of their three stages:
+ * phases bit 1 = ready handshake, 2 = row move, 4 = done handshake (7 = the
+ * whole call).  Lets ranks emulated in one process on one GPU enqueue every
+ * rank's ready stage before any rank's move (the single-GPU tests). */
+ZP_API int zp_remap_push_phased(const void* src, int64_t row_bytes, const int64_t* dst_ptrs,
+                  const int32_t* src_row0, const int32_t* dst_row0, const int32_t* count,
+                  const int64_t* flags_ptrs, const int32_t* expect, int world, int my_rank,
+                  int32_t epoch, int max_count, int phases, void* stream);
+ZP_API int zp_remap_pull_phased(void* dst, int64_t row_bytes, const int64_t* src_ptrs,
+                  const int32_t* src_row0, const int32_t* dst_row0, const int32_t* count,
+                  const int64_t* flags_ptrs, const int32_t* readers, int world, int my_rank,
+                  int32_t epoch, int max_count, int phases, void* stream);
+
+/* Bound of every handshake spin (ready / done flags of the remap): a rank
+ * that waits longer prints the ranks and epochs involved and traps, so a
+ * crashed peer fails the job instead of hanging the GPU.  ms <= 0 restores
+ * the default (30 s).  Returns the previous bound in ms. */
+ZP_API int zp_set_spin_timeout_ms(int64_t ms);
+
 /* Same contract as zp_remap_pull, but the row blocks are moved by the copy
  * engines (one cudaMemcpyAsync per source rank, enqueued between the ready
  * and done handshake kernels), leaving every SM free for concurrent compute.

@@ -9,6 +9,7 @@ results, plus execution entry points that run the plan on B200s
 behind the C ABI in ``include/zeppelin_b200.h``; there is no CPU fallback.
 """
 
+from .baselines import STRATEGIES, plan_hybrid_dp, plan_llama_cp, plan_te_cp
 from .batch import LengthDistribution, SequenceBatch, load_batch, preset, sample_batch, save_batch
 from .cluster import ClusterSpec, ConfigError, single_box
 from .plan import (

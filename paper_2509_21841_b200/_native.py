@@ -35,6 +35,11 @@ SIGNATURES: dict[str, tuple] = {
                                ctypes.c_int32, _c_int, _vp]),
     "zp_remap_pull": (_c_int, [_vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                ctypes.c_int32, _c_int, _vp]),
+    "zp_remap_push_phased": (_c_int, [_vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
+                                      ctypes.c_int32, _c_int, _c_int, _vp]),
+    "zp_remap_pull_phased": (_c_int, [_vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
+                                      ctypes.c_int32, _c_int, _c_int, _vp]),
+    "zp_set_spin_timeout_ms": (_c_int, [_c_i64]),
     "zp_remap_pull_ce": (_c_int, [_vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                   ctypes.c_int32, _vp]),
     "zp_remap_push_ce": (_c_int, [_vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,

@@ -7,32 +7,12 @@
 //                   M[me][d] are stored straight into rank d's landing buffer
 //                   through CUDA-IPC peer pointers (NVLink), then per-pair
 //                   release/acquire flags replace the collective's handshake.
+#include <cstdio>
+
 #include "zp_host.h"
 #include "../../include/zeppelin_b200.h"
 
-#ifndef ZP_PUSH_BULK
-#define ZP_PUSH_BULK 0
-#endif
-
 namespace zp {
-
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init_raw(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_raw(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
 
 constexpr int kMoveThreads = 256;
 constexpr int kUnroll = 4;
@@ -97,65 +77,6 @@ __global__ void __launch_bounds__(kMoveThreads)
   __threadfence_system();
 }
 
-// TMA bulk-copy variant of the push: one elected thread per CTA streams its
-// share of the destination's rows HBM -> SMEM (cp.async.bulk, mbarrier) ->
-// peer HBM (cp.async.bulk.global.shared::cta, bulk groups), kStages deep, so
-// the copy engine path, not SM load/store issue, moves the bytes over NVLink.
-constexpr int kBulkStages = 4;
-constexpr uint32_t kBulkChunk = 32768;
-
-__global__ void __launch_bounds__(32)
-    remap_push_bulk_kernel(const uint8_t* __restrict__ src, int64_t row_bytes,
-                           const int64_t* __restrict__ dst_ptrs, const int32_t* __restrict__ src_row0,
-                           const int32_t* __restrict__ dst_row0, const int32_t* __restrict__ count) {
-  extern __shared__ __align__(128) uint8_t bulk_smem[];
-  __shared__ __align__(8) uint64_t full[kBulkStages];
-  const int d = blockIdx.y;
-  const int64_t n = count[d];
-  if (n <= 0 || threadIdx.x != 0) return;
-  const int64_t bytes = n * row_bytes;
-  const uint8_t* s = src + int64_t(src_row0[d]) * row_bytes;
-  uint8_t* t = reinterpret_cast<uint8_t*>(dst_ptrs[d]) + int64_t(dst_row0[d]) * row_bytes;
-  // contiguous byte range of this CTA (16-byte aligned split)
-  const int64_t per = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~int64_t(15);
-  const int64_t lo = min(bytes, per * int64_t(blockIdx.x));
-  const int64_t hi = min(bytes, lo + per);
-  if (lo >= hi) return;
-  for (int i = 0; i < kBulkStages; ++i) mbar_init_raw(smem_addr(&full[i]), 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  const int64_t nchunks = (hi - lo + kBulkChunk - 1) / kBulkChunk;
-  auto load = [&](int64_t c) {
-    const int st = int(c % kBulkStages);
-    const int64_t off = lo + c * kBulkChunk;
-    const uint32_t len = uint32_t(((hi - off) < int64_t(kBulkChunk) ? (hi - off) : int64_t(kBulkChunk)));
-    const uint32_t bar = smem_addr(&full[st]);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(len) : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_addr(bulk_smem + st * kBulkChunk)),
-        "l"(s + off), "r"(len), "r"(bar)
-        : "memory");
-  };
-  for (int64_t c = 0; c < (nchunks < kBulkStages ? nchunks : int64_t(kBulkStages)); ++c) load(c);
-  for (int64_t c = 0; c < nchunks; ++c) {
-    const int st = int(c % kBulkStages);
-    const int64_t off = lo + c * kBulkChunk;
-    const uint32_t len = uint32_t(((hi - off) < int64_t(kBulkChunk) ? (hi - off) : int64_t(kBulkChunk)));
-    mbar_wait_raw(smem_addr(&full[st]), uint32_t(c / kBulkStages) & 1);
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(t + off),
-                 "r"(smem_addr(bulk_smem + st * kBulkChunk)), "r"(len)
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    if (c + kBulkStages < nchunks) {
-      // the stage is reloaded only after its store has finished reading SMEM
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      load(c + kBulkStages);
-    }
-  }
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  __threadfence_system();
-}
-
 // Pull variant: the receiver reads its incoming rows straight out of the
 // senders' buffers over NVLink (peer LDG.128, L1 no-allocate) and writes them
 // locally.  grid.y = source rank.
@@ -211,19 +132,37 @@ __device__ __forceinline__ int32_t ld_acquire_sys(const int32_t* p) {
   return v;
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Bounded acquire-spin: a peer that never arrives (crashed rank, mismatched
+// epochs) ends in a trap with a message instead of a hung GPU.
+__device__ __forceinline__ void spin_until(const int32_t* f, int32_t epoch, uint64_t timeout_ns,
+                                           const char* what, int me, int peer) {
+  const uint64_t t0 = globaltimer_ns();
+  while (int32_t(uint32_t(ld_acquire_sys(f)) - uint32_t(epoch)) < 0) {
+    if (globaltimer_ns() - t0 > timeout_ns) {
+      printf("zeppelin-b200: %s handshake timed out (rank %d waiting for rank %d, epoch %d, flag %d)\n", what, me,
+             peer, epoch, ld_acquire_sys(f));
+      __trap();
+    }
+  }
+}
+
 // Entry handshake: tell every peer we reached `epoch`, then wait until every
 // rank we are about to store into has reached it too.
 __global__ void remap_ready_kernel(const int64_t* __restrict__ flags_ptrs,
                                    const int32_t* __restrict__ count, int world, int me,
-                                   int32_t epoch) {
+                                   int32_t epoch, uint64_t timeout_ns) {
   __threadfence_system();
   for (int d = threadIdx.x; d < world; d += blockDim.x)
     if (d != me) st_release_sys(reinterpret_cast<int32_t*>(flags_ptrs[d]) + world + me, epoch);
   for (int d = threadIdx.x; d < world; d += blockDim.x) {
     if (d == me || count[d] <= 0) continue;
-    const int32_t* f = reinterpret_cast<const int32_t*>(flags_ptrs[me]) + world + d;
-    while (ld_acquire_sys(f) < epoch) {
-    }
+    spin_until(reinterpret_cast<const int32_t*>(flags_ptrs[me]) + world + d, epoch, timeout_ns, "remap ready", me, d);
   }
 }
 
@@ -232,15 +171,13 @@ __global__ void remap_ready_kernel(const int64_t* __restrict__ flags_ptrs,
 __global__ void remap_done_kernel(const int64_t* __restrict__ flags_ptrs,
                                   const int32_t* __restrict__ count,
                                   const int32_t* __restrict__ expect, int world, int me,
-                                  int32_t epoch) {
+                                  int32_t epoch, uint64_t timeout_ns) {
   __threadfence_system();
   for (int d = threadIdx.x; d < world; d += blockDim.x)
     if (d != me && count[d] > 0) st_release_sys(reinterpret_cast<int32_t*>(flags_ptrs[d]) + me, epoch);
   for (int s = threadIdx.x; s < world; s += blockDim.x) {
     if (s == me || expect[s] == 0) continue;
-    const int32_t* f = reinterpret_cast<const int32_t*>(flags_ptrs[me]) + s;
-    while (ld_acquire_sys(f) < epoch) {
-    }
+    spin_until(reinterpret_cast<const int32_t*>(flags_ptrs[me]) + s, epoch, timeout_ns, "remap done", me, s);
   }
 }
 
@@ -274,46 +211,95 @@ extern "C" int zp_copy_rows(void* dst, int64_t dst_stride_bytes, const void* src
   return ZP_OK;
 }
 
-extern "C" int zp_remap_push(const void* src, int64_t row_bytes, const int64_t* dst_ptrs,
-                             const int32_t* src_row0, const int32_t* dst_row0, const int32_t* count,
-                             const int64_t* flags_ptrs, const int32_t* expect, int world,
-                             int my_rank, int32_t epoch, int max_count, void* stream) {
-  if (world < 1 || world > 64 || my_rank < 0 || my_rank >= world || max_count < 0)
-    return zp_fail(ZP_EINVAL, "zp_remap_push: bad world/rank");
+namespace {
+uint64_t g_spin_timeout_ns = 30ull * 1000000000ull;  // zp_set_spin_timeout_ms
+
+enum : int { kPhaseReady = 1, kPhaseMove = 2, kPhaseDone = 4 };
+
+int launch_ready(const int64_t* flags_ptrs, const int32_t* count, int world, int me, int32_t epoch,
+                 cudaStream_t st, const char* what) {
+  zp::remap_ready_kernel<<<1, 64, 0, st>>>(flags_ptrs, count, world, me, epoch, g_spin_timeout_ns);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ZP_OK : zp_fail_cuda(e, what);
+}
+int launch_done(const int64_t* flags_ptrs, const int32_t* count, const int32_t* expect, int world, int me,
+                int32_t epoch, cudaStream_t st, const char* what) {
+  zp::remap_done_kernel<<<1, 64, 0, st>>>(flags_ptrs, count, expect, world, me, epoch, g_spin_timeout_ns);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ZP_OK : zp_fail_cuda(e, what);
+}
+}  // namespace
+
+extern "C" int zp_set_spin_timeout_ms(int64_t ms) {
+  const uint64_t prev = g_spin_timeout_ns / 1000000ull;
+  g_spin_timeout_ns = ms > 0 ? uint64_t(ms) * 1000000ull : 30ull * 1000000000ull;
+  return int(prev);
+}
+
+extern "C" int zp_remap_push_phased(const void* src, int64_t row_bytes, const int64_t* dst_ptrs,
+                                    const int32_t* src_row0, const int32_t* dst_row0, const int32_t* count,
+                                    const int64_t* flags_ptrs, const int32_t* expect, int world, int my_rank,
+                                    int32_t epoch, int max_count, int phases, void* stream) {
+  if (world < 1 || world > 64 || my_rank < 0 || my_rank >= world || max_count < 0 || phases < 0 || phases > 7)
+    return zp_fail(ZP_EINVAL, "zp_remap_push: bad world/rank/phases");
   if ((reinterpret_cast<uintptr_t>(src) & 15u) || (row_bytes & 15) || row_bytes <= 0)
     return zp_fail(ZP_EINVAL, "zp_remap_push: src and row bytes must be 16-byte aligned");
   if (!dst_ptrs || !src_row0 || !dst_row0 || !count || !flags_ptrs || !expect)
     return zp_fail(ZP_EINVAL, "zp_remap_push: null table");
   if (zp_check_device() != ZP_OK) return ZP_ENODEV;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  zp::remap_ready_kernel<<<1, 64, 0, st>>>(flags_ptrs, count, world, my_rank, epoch);
-  cudaError_t e0 = cudaGetLastError();
-  if (e0 != cudaSuccess) return zp_fail_cuda(e0, "zp_remap_push: ready launch");
-  if (max_count > 0) {
-#if ZP_PUSH_BULK
-    static bool attr = false;
-    const int smem = zp::kBulkStages * int(zp::kBulkChunk);
-    if (!attr) {
-      cudaFuncSetAttribute(zp::remap_push_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr = true;
-    }
-    const int64_t bytes = int64_t(max_count) * row_bytes;
-    int per_dest = int((bytes + (1 << 20) - 1) >> 20);  // ~1 MB per CTA
-    const int cap = 2 * 148 / world + 1;
-    per_dest = per_dest < 1 ? 1 : (per_dest > cap ? cap : per_dest);
-    zp::remap_push_bulk_kernel<<<dim3(per_dest, world), 32, smem, st>>>(
-        reinterpret_cast<const uint8_t*>(src), row_bytes, dst_ptrs, src_row0, dst_row0, count);
-#else
+  int rc;
+  if ((phases & kPhaseReady) &&
+      (rc = launch_ready(flags_ptrs, count, world, my_rank, epoch, st, "zp_remap_push: ready launch")) != ZP_OK)
+    return rc;
+  if ((phases & kPhaseMove) && max_count > 0) {
     dim3 grid(grid_for(int64_t(max_count) * (row_bytes / 16), world), world);
     zp::remap_push_kernel<<<grid, zp::kMoveThreads, 0, st>>>(
         reinterpret_cast<const uint8_t*>(src), row_bytes, dst_ptrs, src_row0, dst_row0, count);
-#endif
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_push: launch");
   }
-  zp::remap_done_kernel<<<1, 64, 0, st>>>(flags_ptrs, count, expect, world, my_rank, epoch);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_push: signal launch");
+  if (phases & kPhaseDone)
+    return launch_done(flags_ptrs, count, expect, world, my_rank, epoch, st, "zp_remap_push: signal launch");
+  return ZP_OK;
+}
+
+extern "C" int zp_remap_push(const void* src, int64_t row_bytes, const int64_t* dst_ptrs,
+                             const int32_t* src_row0, const int32_t* dst_row0, const int32_t* count,
+                             const int64_t* flags_ptrs, const int32_t* expect, int world,
+                             int my_rank, int32_t epoch, int max_count, void* stream) {
+  return zp_remap_push_phased(src, row_bytes, dst_ptrs, src_row0, dst_row0, count, flags_ptrs, expect, world,
+                              my_rank, epoch, max_count, 7, stream);
+}
+
+extern "C" int zp_remap_pull_phased(void* dst, int64_t row_bytes, const int64_t* src_ptrs,
+                                    const int32_t* src_row0, const int32_t* dst_row0, const int32_t* count,
+                                    const int64_t* flags_ptrs, const int32_t* readers, int world, int my_rank,
+                                    int32_t epoch, int max_count, int phases, void* stream) {
+  if (world < 1 || world > 64 || my_rank < 0 || my_rank >= world || max_count < 0 || phases < 0 || phases > 7)
+    return zp_fail(ZP_EINVAL, "zp_remap_pull: bad world/rank/phases");
+  if ((reinterpret_cast<uintptr_t>(dst) & 15u) || (row_bytes & 15) || row_bytes <= 0)
+    return zp_fail(ZP_EINVAL, "zp_remap_pull: dst and row bytes must be 16-byte aligned");
+  if (!src_ptrs || !src_row0 || !dst_row0 || !count || !flags_ptrs || !readers)
+    return zp_fail(ZP_EINVAL, "zp_remap_pull: null table");
+  if (zp_check_device() != ZP_OK) return ZP_ENODEV;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int rc;
+  // ready: my source rows are final for this epoch; wait for my sources (count > 0)
+  if ((phases & kPhaseReady) &&
+      (rc = launch_ready(flags_ptrs, count, world, my_rank, epoch, st, "zp_remap_pull: ready launch")) != ZP_OK)
+    return rc;
+  if ((phases & kPhaseMove) && max_count > 0) {
+    dim3 grid(grid_for(int64_t(max_count) * (row_bytes / 16), world), world);
+    zp::remap_pull_kernel<<<grid, zp::kMoveThreads, 0, st>>>(reinterpret_cast<uint8_t*>(dst), row_bytes,
+                                                             src_ptrs, src_row0, dst_row0, count);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_pull: launch");
+  }
+  // done: tell each source I finished reading it; wait until every reader of my
+  // rows finished, so the caller may overwrite them
+  if (phases & kPhaseDone)
+    return launch_done(flags_ptrs, count, readers, world, my_rank, epoch, st, "zp_remap_pull: done launch");
   return ZP_OK;
 }
 
@@ -321,31 +307,8 @@ extern "C" int zp_remap_pull(void* dst, int64_t row_bytes, const int64_t* src_pt
                              const int32_t* src_row0, const int32_t* dst_row0, const int32_t* count,
                              const int64_t* flags_ptrs, const int32_t* readers, int world,
                              int my_rank, int32_t epoch, int max_count, void* stream) {
-  if (world < 1 || world > 64 || my_rank < 0 || my_rank >= world || max_count < 0)
-    return zp_fail(ZP_EINVAL, "zp_remap_pull: bad world/rank");
-  if ((reinterpret_cast<uintptr_t>(dst) & 15u) || (row_bytes & 15) || row_bytes <= 0)
-    return zp_fail(ZP_EINVAL, "zp_remap_pull: dst and row bytes must be 16-byte aligned");
-  if (!src_ptrs || !src_row0 || !dst_row0 || !count || !flags_ptrs || !readers)
-    return zp_fail(ZP_EINVAL, "zp_remap_pull: null table");
-  if (zp_check_device() != ZP_OK) return ZP_ENODEV;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  // ready: my source rows are final for this epoch; wait for my sources (count > 0)
-  zp::remap_ready_kernel<<<1, 64, 0, st>>>(flags_ptrs, count, world, my_rank, epoch);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_pull: ready launch");
-  if (max_count > 0) {
-    dim3 grid(grid_for(int64_t(max_count) * (row_bytes / 16), world), world);
-    zp::remap_pull_kernel<<<grid, zp::kMoveThreads, 0, st>>>(reinterpret_cast<uint8_t*>(dst), row_bytes,
-                                                             src_ptrs, src_row0, dst_row0, count);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_pull: launch");
-  }
-  // done: tell each source I finished reading it; wait until every reader of my
-  // rows finished, so the caller may overwrite them
-  zp::remap_done_kernel<<<1, 64, 0, st>>>(flags_ptrs, count, readers, world, my_rank, epoch);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_pull: done launch");
-  return ZP_OK;
+  return zp_remap_pull_phased(dst, row_bytes, src_ptrs, src_row0, dst_row0, count, flags_ptrs, readers, world,
+                              my_rank, epoch, max_count, 7, stream);
 }
 
 extern "C" int zp_remap_pull_ce(void* dst, int64_t row_bytes, const int64_t* src_ptrs_host,
@@ -360,9 +323,9 @@ extern "C" int zp_remap_pull_ce(void* dst, int64_t row_bytes, const int64_t* src
     return zp_fail(ZP_EINVAL, "zp_remap_pull_ce: null table");
   if (zp_check_device() != ZP_OK) return ZP_ENODEV;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  zp::remap_ready_kernel<<<1, 64, 0, st>>>(flags_ptrs, count_dev, world, my_rank, epoch);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_pull_ce: ready launch");
+  int rc = launch_ready(flags_ptrs, count_dev, world, my_rank, epoch, st, "zp_remap_pull_ce: ready launch");
+  if (rc != ZP_OK) return rc;
+  cudaError_t e;
   for (int s = 0; s < world; ++s) {
     if (count_host[s] <= 0) continue;
     e = cudaMemcpyAsync(reinterpret_cast<uint8_t*>(dst) + int64_t(dst_row0_host[s]) * row_bytes,
@@ -370,10 +333,7 @@ extern "C" int zp_remap_pull_ce(void* dst, int64_t row_bytes, const int64_t* src
                         size_t(count_host[s]) * size_t(row_bytes), cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_pull_ce: copy");
   }
-  zp::remap_done_kernel<<<1, 64, 0, st>>>(flags_ptrs, count_dev, readers_dev, world, my_rank, epoch);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_pull_ce: done launch");
-  return ZP_OK;
+  return launch_done(flags_ptrs, count_dev, readers_dev, world, my_rank, epoch, st, "zp_remap_pull_ce: done launch");
 }
 
 extern "C" int zp_remap_push_ce(const void* src, int64_t row_bytes, const int64_t* dst_ptrs_host,
@@ -388,9 +348,9 @@ extern "C" int zp_remap_push_ce(const void* src, int64_t row_bytes, const int64_
     return zp_fail(ZP_EINVAL, "zp_remap_push_ce: null table");
   if (zp_check_device() != ZP_OK) return ZP_ENODEV;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  zp::remap_ready_kernel<<<1, 64, 0, st>>>(flags_ptrs, count_dev, world, my_rank, epoch);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_push_ce: ready launch");
+  int rc = launch_ready(flags_ptrs, count_dev, world, my_rank, epoch, st, "zp_remap_push_ce: ready launch");
+  if (rc != ZP_OK) return rc;
+  cudaError_t e;
   for (int d = 0; d < world; ++d) {
     if (count_host[d] <= 0) continue;
     e = cudaMemcpyAsync(reinterpret_cast<uint8_t*>(dst_ptrs_host[d]) + int64_t(dst_row0_host[d]) * row_bytes,
@@ -398,8 +358,5 @@ extern "C" int zp_remap_push_ce(const void* src, int64_t row_bytes, const int64_
                         size_t(count_host[d]) * size_t(row_bytes), cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_push_ce: copy");
   }
-  zp::remap_done_kernel<<<1, 64, 0, st>>>(flags_ptrs, count_dev, expect_dev, world, my_rank, epoch);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_remap_push_ce: done launch");
-  return ZP_OK;
+  return launch_done(flags_ptrs, count_dev, expect_dev, world, my_rank, epoch, st, "zp_remap_push_ce: done launch");
 }

@@ -36,17 +36,12 @@ import torch.distributed as dist
 from . import ops
 from .plan import build_plan
 from .program import BwdProgram, RankProgram, build_bwd_program, build_rank_program
-from .remap import RemapLayout, remap_layout
+from .remap import RemapLayout, cost_matrix, remap_layout, solve_remap
 from .schedule import build_schedule
 from .worklist import BwdWorkList, WorkList
 
 
-# SMs a ring round's attention launch leaves free while the next KV hop is in
-# flight, and the CTA cap of the ring communicator: NCCL's P2P kernels need
-# SMs, and a persistent kernel holding all of them queues the hop behind the
-# whole round.  Measured at N=4 (C3): step 52.7 -> 50.8 ms with 4 SMs / 2 CTAs.
-RING_SM_RESERVE = int(os.environ.get("ZP_RING_SM_RESERVE", "4"))
-RING_NCCL_CTAS = int(os.environ.get("ZP_RING_NCCL_CTAS", "2"))
+_CONTEXTS: dict = {}
 
 
 class RankContext:
@@ -60,20 +55,13 @@ class RankContext:
         self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.group = group
         self.comm_stream = torch.cuda.Stream(self.device) if world > 1 else None
-        # forward ring KV hops go through their own NCCL communicator capped at
-        # RING_NCCL_CTAS CTAs, so they fit in the SMs a ring round leaves free
-        # (RING_SM_RESERVE) and overlap the round instead of queueing behind it;
-        # the backward's (non-persistent kernel, larger fp32 partials) stay on
-        # the uncapped group
-        self.ring_group = group
-        if world > 1 and dist.is_available() and dist.is_initialized() and RING_NCCL_CTAS > 0:
-            opts = dist.ProcessGroupNCCL.Options()
-            opts.config.max_ctas = RING_NCCL_CTAS
-            opts.config.min_ctas = 1
-            ranks = dist.get_process_group_ranks(group) if group is not None else list(range(world))
-            self.ring_group = dist.new_group(ranks=ranks, backend="nccl", pg_options=opts)
         self._ws: dict[str, torch.Tensor] = {}
         self.tracer = None  # trace.Tracer: measured timeline in the reference trace schema
+        # ring KV exchange (RingTransport): buffers + flags reachable by the peers,
+        # and the epoch base of the next attention call (advanced identically on
+        # every rank: the schedule is the same everywhere)
+        self.ring: RingTransport | None = None
+        self.ring_epoch = 16
 
     def span(self, stream_name: str, kind: str, payload: dict | None = None, stream=None):
         import contextlib
@@ -83,9 +71,18 @@ class RankContext:
 
     @classmethod
     def from_env(cls) -> "RankContext":
+        """The process's context for the default group on the current device
+        (one per (rank, world, device), reused across calls: a context owns
+        streams, workspaces and the IPC-registered ring buffers)."""
         if dist.is_available() and dist.is_initialized():
-            return cls(dist.get_rank(), dist.get_world_size())
-        return cls()
+            key = (dist.get_rank(), dist.get_world_size(), torch.cuda.current_device())
+        else:
+            key = (0, 1, torch.cuda.current_device())
+        ctx = _CONTEXTS.get(key)
+        if ctx is None:
+            ctx = cls(key[0], key[1], torch.device("cuda", key[2]))
+            _CONTEXTS[key] = ctx
+        return ctx
 
     def workspace(self, name: str, shape, dtype) -> torch.Tensor:
         numel = int(np.prod(shape))
@@ -110,9 +107,13 @@ class TableStager:
     on the compute stream ties the host to the device's progress and breaks
     host-fed pipelines.  Here K slots rotate; each upload is a copy on a
     private stream that waits only for the kernels that read the slot K
-    uploads ago (an event recorded on the compute stream at the next upload,
-    i.e. after those kernels were enqueued); the compute stream waits for the
-    copy.  The host blocks only if it runs K uploads ahead of the device."""
+    uploads ago; the compute stream waits for the copy.  The host blocks only
+    if it runs K uploads ahead of the device.
+
+    A slot counts as consumed when ``release()`` is called (the caller has
+    enqueued every kernel that reads it) or, failing that, at the next
+    upload — so a caller that uploads several tables for one step must pack
+    them into one upload or release explicitly after the readers."""
 
     def __init__(self, device: torch.device, slots: int = 3):
         self.device = device
@@ -121,12 +122,17 @@ class TableStager:
         self.prev = None
         self.stream = torch.cuda.Stream(device)
 
+    def release(self) -> None:
+        """Every reader of the latest upload is enqueued on the current stream."""
+        if self.prev is not None and not self.prev["released"]:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(self.device))
+            self.prev["consumed"] = ev
+            self.prev["released"] = True
+
     def upload(self, host: np.ndarray) -> torch.Tensor:
         cs = torch.cuda.current_stream(self.device)
-        if self.prev is not None:  # kernels reading the previous upload are enqueued by now
-            ev = torch.cuda.Event()
-            ev.record(cs)
-            self.prev["consumed"] = ev
+        self.release()  # implicit: readers of the previous upload are enqueued by now
         n = host.size
         slot = self.slots[self.turn]
         self.turn = (self.turn + 1) % len(self.slots)
@@ -134,7 +140,7 @@ class TableStager:
             cap = max(n, 1 << 16)
             slot = {"pin": torch.empty(cap, dtype=torch.int32).pin_memory(),
                     "dev": torch.empty(cap, dtype=torch.int32, device=self.device),
-                    "copied": None, "consumed": torch.cuda.Event()}
+                    "copied": None, "consumed": torch.cuda.Event(), "released": False}
             # the new block comes from the compute stream's pool: kernels still
             # in flight there may have used this memory — the copy waits for them
             slot["consumed"].record(cs)
@@ -150,6 +156,7 @@ class TableStager:
             done = torch.cuda.Event()
             done.record(self.stream)
         slot["copied"] = done
+        slot["released"] = False
         cs.wait_event(done)
         self.prev = slot
         return dev
@@ -208,65 +215,159 @@ def ring_p2p_ops(rp, round_index: int, cur: torch.Tensor, nxt: torch.Tensor, gro
 
 
 
-def _run_ring(ctx: RankContext, rp, dev_pack, dev_rounds, q, k, v, o, lse, scale):
+class RingTransport:
+    """One rank's ring KV buffers and epoch flags, plus the peers' addresses.
+
+    ``n_buf`` buffers of ``rows`` KV rows (K and V interleaved per row, 4 KiB
+    per token at Llama-3 shapes) in one allocation, and an int32 flag block
+    ``[0, world)`` "full from predecessor p", ``[world, 2*world)`` "consumed by
+    successor s".  Peers reach both over NVLink through CUDA IPC
+    (``create``, collective), or — ranks emulated in one process on one GPU —
+    through plain device pointers (``local_group``).  The hop itself is
+    ``zp_ring_hop``: stream-ordered flag waits / writes and one copy-engine
+    pull, no SM (RingHop describes the protocol)."""
+
+    N_BUF = 3
+
+    def __init__(self, ctx: RankContext, rows: int, row_bytes: int):
+        self.ctx = ctx
+        self.rows, self.row_bytes = rows, row_bytes
+        self.storage = torch.empty(self.N_BUF * max(rows, 1) * row_bytes, dtype=torch.uint8, device=ctx.device)
+        self.flags = torch.zeros(2 * ctx.world, dtype=torch.int32, device=ctx.device)
+        self.buf_base: list[int] = []   # per rank: address of its storage (this process's mapping)
+        self.flag_base: list[int] = []  # per rank: address of its flag block
+
+    def fits(self, rows: int, row_bytes: int) -> bool:
+        return rows <= self.rows and row_bytes == self.row_bytes
+
+    @classmethod
+    def create(cls, ctx: RankContext, rows: int, row_bytes: int) -> "RingTransport":
+        """Collective over ctx.group: allocate and exchange IPC handles."""
+        t = cls(ctx, rows, row_bytes)
+        torch.cuda.synchronize(ctx.device)
+        mine = (_ipc_export(t.storage), _ipc_export(t.flags))
+        everyone = [None] * ctx.world
+        dist.all_gather_object(everyone, mine, group=ctx.group)
+        for r, ((bh, bo), (fh, fo)) in enumerate(everyone):
+            if r == ctx.rank:
+                t.buf_base.append(t.storage.data_ptr())
+                t.flag_base.append(t.flags.data_ptr())
+            else:
+                t.buf_base.append(_ipc_open(bh, bo))
+                t.flag_base.append(_ipc_open(fh, fo))
+        dist.barrier(group=ctx.group)
+        return t
+
+    @classmethod
+    def local_group(cls, ctxs: list[RankContext], rows: int, row_bytes: int) -> list["RingTransport"]:
+        """Emulated ranks on one device: peers' buffers are local pointers."""
+        ts = [cls(c, rows, row_bytes) for c in ctxs]
+        for t in ts:
+            t.buf_base = [x.storage.data_ptr() for x in ts]
+            t.flag_base = [x.flags.data_ptr() for x in ts]
+        return ts
+
+    def buffer(self, j: int, hkv: int, d: int) -> torch.Tensor:
+        n = self.rows * self.row_bytes
+        return self.storage[j * n:(j + 1) * n].view(torch.bfloat16).view(self.rows, 2, hkv, d)
+
+    def buf_addr(self, rank: int, j: int) -> int:
+        return self.buf_base[rank] + j * self.rows * self.row_bytes
+
+    def full_flag(self, owner: int, sender: int) -> int:
+        """Address of owner's "full from sender" flag."""
+        return self.flag_base[owner] + 4 * sender
+
+    def consumed_flag(self, owner: int, reader: int) -> int:
+        """Address of owner's "consumed by reader" flag."""
+        return self.flag_base[owner] + 4 * (self.ctx.world + reader)
+
+
+def ring_rows_needed(schedule) -> int:
+    """KV buffer rows every rank allocates: the largest set any position of
+    any ring holds (identical on every rank: taken from the global schedule,
+    so a growth re-exchange is entered collectively)."""
+    return max((rs.ring.kv_tokens(p) for rs in schedule.rings() for p in range(rs.ring.group_size)), default=0)
+
+
+def _ensure_ring_transport(ctx: RankContext, schedule, hkv: int, d: int) -> RingTransport:
+    rows = ring_rows_needed(schedule)
+    row_bytes = 2 * hkv * d * 2
+    if ctx.ring is None or not ctx.ring.fits(rows, row_bytes):
+        grow = rows if ctx.ring is None else max(rows, int(1.25 * ctx.ring.rows))
+        ctx.ring = RingTransport.create(ctx, grow, row_bytes)
+    return ctx.ring
+
+
+def _ring_steps(ctx: RankContext, rp, epoch0: int, dev_pack, dev_rounds, q, k, v, o, lse, scale):
+    """One ring at this position, as a generator: yields after the pack and
+    after each round is enqueued (the single-GPU emulation interleaves the
+    members' generators step by step, so every flag wait is enqueued after
+    the write it waits for).  Compute on the current stream, hops on the
+    context's comm stream (copy engines; no SM is taken from the rounds).
+
+    Per round r: attention of this position's query rows against the KV set
+    held from position (i - r) mod g (reference attention_engine.py:229-244),
+    resuming the running softmax state; hop r pulls the next set from the
+    predecessor (attention_engine.py:247-251) while round r runs."""
+    from . import _native
+    T = ctx.ring
     hkv, d = k.shape[1], k.shape[2]
     hq = q.shape[1]
-    cs = torch.cuda.current_stream()
+    g, me, pred, succ = rp.group_size, ctx.rank, rp.prev_rank, rp.next_rank
     xs = ctx.comm_stream
-    rows = max(rp.held_rows)
-    # three KV buffers: the hop that fills round r+1's buffer waits only for
-    # round r-2 (its last reader), so KV sets travel around the ring at link
-    # speed instead of in lockstep with the slowest member's compute
-    nbuf = 3 if rp.group_size > 2 else 2
-    bufs = [ctx.workspace(f"ringkv{j}", (rows, 2, hkv, d), torch.bfloat16) for j in range(nbuf)]
+    parity = v.dtype == torch.float16
+    bufs = [T.buffer(j, hkv, d) for j in range(rp.n_buffers)]
     st_o = ctx.workspace("ring_state_o", (max(rp.state_rows, 1), hq, d), torch.float32)
     st_ml = ctx.workspace("ring_state_ml", (2, hq, max(rp.state_rows, 1)), torch.float32)
     n_pack = rp.pack_ranges.shape[0]
     max_pack = int(rp.pack_ranges[:, 2].max()) if n_pack else 0
+    cs = torch.cuda.current_stream()
+    # own set -> buffer 0, announced to the successor (epoch offset 0)
     ops.copy_rows(bufs[0][:, 0], k, dev_pack, n_pack, max_pack)
     ops.copy_rows(bufs[0][:, 1], v, dev_pack, n_pack, max_pack)
-    ready = torch.cuda.Event()
-    ready.record(cs)
-    done_at: dict[int, torch.cuda.Event] = {}
-    g = rp.group_size
+    _native.call("zp_stream_write_flag", T.full_flag(succ, me), epoch0, int(cs.cuda_stream))
+    yield
+    hops = rp.hops()
+    ready: dict[int, torch.cuda.Event] = {}
+    done: dict[int, torch.cuda.Event] = {}
     for r in range(g):
-        cur, nxt = bufs[r % nbuf], bufs[(r + 1) % nbuf]
-        nxt_ready = None
+        cs = torch.cuda.current_stream()
         if r < g - 1:
-            xs.wait_event(ready)
-            last_reader = r + 1 - nbuf  # the round that last read nxt
-            if last_reader >= 0:
-                xs.wait_event(done_at[last_reader])
-            with torch.cuda.stream(xs), ctx.span("intra-comm", "kv.send",
-                                                  {"ring": rp.ring_index, "round": r, "tokens": rp.send_rows(r),
-                                                   "dst": rp.next_rank}, xs):
-                p2p = ring_p2p_ops(rp, r, cur, nxt, ctx.ring_group)
-                if p2p:
-                    for req in dist.batch_isend_irecv(p2p):
-                        req.wait()
-            nxt_ready = torch.cuda.Event()
-            nxt_ready.record(xs)
+            h = hops[r]
+            if h.free is not None:
+                xs.wait_event(done[h.free])  # the dst buffer's last local reader
+            with ctx.span("intra-comm", "kv.send", {"ring": rp.ring_index, "round": r, "tokens": h.rows,
+                                                     "src": pred}, xs):
+                _native.call("zp_ring_hop", T.buf_addr(me, h.dst_buf), T.buf_addr(pred, h.src_buf),
+                             h.rows * T.row_bytes, T.full_flag(me, pred), epoch0 + h.full,
+                             T.consumed_flag(me, succ) if h.free is not None else None,
+                             epoch0 + (h.free or 0), T.consumed_flag(pred, me), epoch0 + h.consumed,
+                             T.full_flag(succ, me) if h.next_full is not None else None,
+                             epoch0 + (h.next_full or 0), int(xs.cuda_stream))
+            ev = torch.cuda.Event()
+            ev.record(xs)
+            ready[r + 1] = ev
         if r > 0:
-            cs.wait_event(ready)
+            cs.wait_event(ready[r])
         work = dev_rounds[r]
+        buf = bufs[r % rp.n_buffers]
         n_kv = rp.rounds[r].kv_rows
         with ctx.span("compute", "intra_node.attn",
                       {"ring": rp.ring_index, "round": r, "pairs": rp.rounds[r].work.pairs_per_head}):
             if work.n:
-                # while the next hop is in flight, leave SMs to its P2P kernels
-                prev = ops.set_sm_reserve(RING_SM_RESERVE if nxt_ready is not None else 0)
-                try:
-                    ops.attn_fwd(q, cur[:n_kv, 0], cur[:n_kv, 1], work.items, work.n, work.segs, o, lse,
-                                 st_o, st_ml, softmax_scale=scale)
-                finally:
-                    ops.set_sm_reserve(prev)
-        done = torch.cuda.Event()
-        done.record(cs)
-        done_at[r] = done
-        if nxt_ready is not None:
-            ready = nxt_ready
-    if xs is not None:
-        cs.wait_stream(xs)  # buffers / sends complete before the next ring reuses them
+                vv = buf[:n_kv, 1].view(torch.float16) if parity else buf[:n_kv, 1]
+                ops.attn_fwd(q, buf[:n_kv, 0], vv, work.items, work.n, work.segs, o, lse, st_o, st_ml,
+                             softmax_scale=scale)
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        done[r] = ev
+        yield
+    # leave the ring only after the successor pulled its last set from us
+    # (the next ring refills buffer 0); rounds after this wait on the stream
+    if g >= 2:
+        _native.call("zp_stream_wait_flag", T.consumed_flag(me, succ), epoch0 + g - 2, int(xs.cuda_stream))
+    torch.cuda.current_stream().wait_stream(xs)
 
 
 def _run_ring_allgather(ctx: RankContext, rp, dev_pack, dev_rounds, q, k, v, o, lse, scale):
@@ -298,6 +399,27 @@ def _run_ring_allgather(ctx: RankContext, rp, dev_pack, dev_rounds, q, k, v, o, 
                          st_o, st_ml, softmax_scale=scale)
 
 
+def attention_steps(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, ctx: RankContext,
+                    prog: RankProgram, devp: "DeviceProgram", o: torch.Tensor, lse: torch.Tensor, scale: float,
+                    kv_exchange: str = "ring"):
+    """Generator form of ``attention_forward``: yields ``(ring_index, step)``
+    after each ring step (pack = step 0, round r = step r+1).  Rings run in
+    ``schedule.rings()`` order on every rank (reference attention_engine.py:
+    266-271), each position pulling the next KV set while it computes."""
+    epoch = ctx.ring_epoch
+    ctx.ring_epoch += 16 * len(schedule.rings())  # the same on every rank
+    if devp.local.n:
+        with ctx.span("compute", "local.attn", {"pairs": prog.local.pairs_per_head, "items": devp.local.n}):
+            ops.attn_fwd(q, k, v, devp.local.items, devp.local.n, devp.local.segs, o, lse, softmax_scale=scale)
+    for rp, (pack, rounds) in zip(prog.rings, devp.rings):
+        if kv_exchange == "allgather":
+            _run_ring_allgather(ctx, rp, pack, rounds, q, k, v, o, lse, scale)
+            continue
+        for step, _ in enumerate(_ring_steps(ctx, rp, epoch + 16 * rp.ring_index, pack, rounds, q, k, v, o,
+                                             lse, scale)):
+            yield rp.ring_index, step
+
+
 def attention_forward(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
                       ctx: RankContext | None = None, program: RankProgram | None = None,
                       device_program: DeviceProgram | None = None, softmax_scale: float | None = None,
@@ -306,7 +428,9 @@ def attention_forward(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torch
 
     q [A_r, Hq, 128], k/v [A_r, Hkv, 128] bf16 in the rank's attention layout
     (plan.fragments[rank] rows in order).  Returns (o [A_r, Hq, 128] bf16,
-    lse [Hq, A_r] fp32)."""
+    lse [Hq, A_r] fp32).  With an fp16 v the parity mode runs (fp16 P/V,
+    fp32 o; ``zp_attn_fwd_parity``).  Collective when the plan has rings:
+    every rank of the context calls it with the same plan."""
     ctx = ctx or RankContext.from_env()
     hq = q.shape[1]
     prog = program or build_rank_program(plan, schedule, ctx.rank, hq)
@@ -315,16 +439,14 @@ def attention_forward(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torch
     devp = device_program or DeviceProgram(prog, q.device)
     scale = 1.0 / math.sqrt(q.shape[2]) if softmax_scale is None else softmax_scale
     if out is None:
-        o = torch.empty_like(q)
+        o = torch.empty(q.shape, dtype=torch.float32 if v.dtype == torch.float16 else q.dtype, device=q.device)
         lse = torch.empty(hq, max(prog.rows, 1), dtype=torch.float32, device=q.device)
     else:
         o, lse = out
-    if devp.local.n:
-        with ctx.span("compute", "local.attn", {"pairs": prog.local.pairs_per_head, "items": devp.local.n}):
-            ops.attn_fwd(q, k, v, devp.local.items, devp.local.n, devp.local.segs, o, lse, softmax_scale=scale)
-    run = _run_ring_allgather if kv_exchange == "allgather" else _run_ring
-    for rp, (pack, rounds) in zip(prog.rings, devp.rings):
-        run(ctx, rp, pack, rounds, q, k, v, o, lse, scale)
+    if ctx.world > 1 and schedule.rings() and kv_exchange == "ring":
+        _ensure_ring_transport(ctx, schedule, k.shape[1], k.shape[2])
+    for _ in attention_steps(plan, schedule, q, k, v, ctx, prog, devp, o, lse, scale, kv_exchange):
+        pass
     return o, lse
 
 
@@ -497,10 +619,12 @@ def _copy_prefix(dst: torch.Tensor, src: torch.Tensor, n: int, ctx: RankContext)
     ops.copy_rows(dst, src, host.to(dst.device, non_blocking=True), 1, n)
 
 
-def _remap_move(ctx: RankContext, src: torch.Tensor, dst: torch.Tensor, slices) -> None:
+def _remap_move(ctx: RankContext, src: torch.Tensor, dst: torch.Tensor, slices, moved: int) -> None:
     kept, (s_lo, s_hi), (r_lo, r_hi), send, recv = slices
     _copy_prefix(dst, src, kept, ctx)
-    if any(send) or any(recv):
+    # every rank enters (or skips) the collective together: the decision uses
+    # the layout's global row count, never this rank's own send / recv
+    if moved > 0:
         _all_to_all(ctx, dst[r_lo:r_hi], src[s_lo:s_hi], recv, send)
 
 
@@ -516,7 +640,7 @@ def remap_forward(layout: RemapLayout, x: torch.Tensor, ctx: RankContext | None 
     if x.shape[0] != a:
         raise ValueError(f"rank {ctx.rank}: remap input has {x.shape[0]} rows, layout says {a}")
     y = out if out is not None else torch.empty((b,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
-    _remap_move(ctx, x, y, layout.forward_slices(ctx.rank))
+    _remap_move(ctx, x, y, layout.forward_slices(ctx.rank), layout.moved_rows())
     return y
 
 
@@ -528,7 +652,7 @@ def remap_inverse(layout: RemapLayout, y: torch.Tensor, ctx: RankContext | None 
     if y.shape[0] != b:
         raise ValueError(f"rank {ctx.rank}: remap input has {y.shape[0]} rows, layout says {b}")
     x = out if out is not None else torch.empty((a,) + tuple(y.shape[1:]), dtype=y.dtype, device=y.device)
-    _remap_move(ctx, y, x, layout.inverse_slices(ctx.rank))
+    _remap_move(ctx, y, x, layout.inverse_slices(ctx.rank), layout.moved_rows())
     return x
 
 
@@ -590,6 +714,26 @@ class PeerBuffer:
     def row_bytes(self) -> int:
         return self.buf.shape[1] * self.buf.element_size()
 
+    @classmethod
+    def local_group(cls, ctxs: list[RankContext], rows: int, row_elems: int, dtype=torch.bfloat16):
+        """Emulated ranks on one device: every peer pointer is a local one
+        (same kernels and handshakes as the IPC-mapped buffers)."""
+        out = []
+        for c in ctxs:
+            pb = cls.__new__(cls)
+            pb.ctx = c
+            pb.buf = torch.empty(max(rows, 1), row_elems, dtype=dtype, device=c.device)
+            pb.flags = torch.zeros(2 * c.world, dtype=torch.int32, device=c.device)
+            pb.epoch = 0
+            pb.host_ptrs = None
+            out.append(pb)
+        ptrs = [pb.buf.data_ptr() for pb in out]
+        fptrs = [pb.flags.data_ptr() for pb in out]
+        for pb in out:
+            pb.peer_ptrs = torch.tensor(ptrs, dtype=torch.int64, device=pb.buf.device)
+            pb.flag_ptrs = torch.tensor(fptrs, dtype=torch.int64, device=pb.buf.device)
+        return out
+
 
 @dataclass
 class _PushTables:
@@ -619,7 +763,7 @@ def push_tables(layout: RemapLayout, rank: int, inverse: bool, device) -> _PushT
 
 def remap_push(layout: RemapLayout, x: torch.Tensor, peer: PeerBuffer, ctx: RankContext,
                inverse: bool = False, tables: _PushTables | None = None,
-               copy_engine: bool = False) -> torch.Tensor:
+               copy_engine: bool = False, phases: int = 7) -> torch.Tensor:
     """Fused remap: this rank's outgoing rows are stored straight into the
     receivers' ``peer`` buffers (one kernel, NVLink peer stores, ready/done
     epoch flags) — the all-to-allv without a collective library.  Kept rows
@@ -633,11 +777,13 @@ def remap_push(layout: RemapLayout, x: torch.Tensor, peer: PeerBuffer, ctx: Rank
     if x.shape[0] != rows_in:
         raise ValueError(f"rank {r}: remap input has {x.shape[0]} rows, layout says {rows_in}")
     out = peer.buf[:rows_out]
-    _copy_prefix(out, x, min(a, b), ctx)
+    if phases & 1:
+        _copy_prefix(out, x, min(a, b), ctx)
     if layout.moved_rows() == 0:
         return out
     tb = tables or push_tables(layout, r, inverse, x.device)
-    peer.epoch += 1
+    if phases & 1:
+        peer.epoch += 1
     t = tb.table
     if copy_engine:
         if peer.host_ptrs is None:
@@ -649,12 +795,38 @@ def remap_push(layout: RemapLayout, x: torch.Tensor, peer: PeerBuffer, ctx: Rank
                      t[2].data_ptr(), t[3].data_ptr(), ctx.world, r, peer.epoch,
                      int(torch.cuda.current_stream().cuda_stream))
         return out
-    ops._count_launch(3)
-    _native.call("zp_remap_push", x.data_ptr(), peer.row_bytes, peer.peer_ptrs.data_ptr(),
+    ops._count_launch(bin(phases).count("1"))
+    _native.call("zp_remap_push_phased", x.data_ptr(), peer.row_bytes, peer.peer_ptrs.data_ptr(),
                  t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), peer.flag_ptrs.data_ptr(),
-                 t[3].data_ptr(), ctx.world, r, peer.epoch, tb.max_count,
+                 t[3].data_ptr(), ctx.world, r, peer.epoch, tb.max_count, phases,
                  int(torch.cuda.current_stream().cuda_stream))
     return out
+
+
+def _pull_host(layout: RemapLayout, rank: int, inverse: bool) -> np.ndarray:
+    w = layout.world
+    m = layout.matrix
+    if not inverse:
+        count = [int(m[s, rank]) for s in range(w)]
+        src0 = [layout.send_offsets(s)[rank] for s in range(w)]
+        dst0 = layout.recv_offsets(rank)
+        readers = [int(m[rank, d] > 0) for d in range(w)]
+    else:
+        count = [int(m[rank, d]) for d in range(w)]
+        src0 = [layout.recv_offsets(d)[rank] for d in range(w)]
+        dst0 = layout.send_offsets(rank)
+        readers = [int(m[s, rank] > 0) for s in range(w)]
+    return np.asarray([src0, dst0, count, readers], dtype=np.int32)
+
+
+def pull_table_pair(layout: RemapLayout, rank: int, stager: TableStager) -> tuple[_PushTables, _PushTables]:
+    """Forward and inverse pull tables of one step in ONE staged upload (so
+    the stager's slot is consumed only after both remaps were enqueued)."""
+    fw, inv = _pull_host(layout, rank, False), _pull_host(layout, rank, True)
+    w = layout.world
+    dev = stager.upload(np.concatenate([fw.reshape(-1), inv.reshape(-1)])).view(2, 4, w)
+    return (_PushTables(dev[0], int(fw[2].max()) if w else 0, np.ascontiguousarray(fw)),
+            _PushTables(dev[1], int(inv[2].max()) if w else 0, np.ascontiguousarray(inv)))
 
 
 def pull_tables(layout: RemapLayout, rank: int, inverse: bool, device,
@@ -682,21 +854,24 @@ def pull_tables(layout: RemapLayout, rank: int, inverse: bool, device,
 
 def remap_pull(layout: RemapLayout, src: PeerBuffer, out: torch.Tensor, ctx: RankContext,
                inverse: bool = False, tables: _PushTables | None = None,
-               copy_engine: bool = False) -> torch.Tensor:
+               copy_engine: bool = False, phases: int = 7) -> torch.Tensor:
     """Fused remap, pull form: this rank reads its incoming rows straight from
     the senders' IPC-shared buffers (``src``: attention layout for forward,
-    linear layout for inverse) over NVLink into ``out``."""
+    linear layout for inverse) over NVLink into ``out``.  ``phases`` (bit 1
+    ready, 2 move, 4 done) splits the call for ranks emulated on one GPU."""
     from . import _native
     r = ctx.rank
     a, b = layout.attn_rows[r], layout.linear_rows[r]
     rows_in, rows_out = (b, a) if inverse else (a, b)
     if out.shape[0] < rows_out:
         raise ValueError(f"rank {r}: remap output needs {rows_out} rows")
-    _copy_prefix(out, src.buf[:rows_in], min(a, b), ctx)
+    if phases & 1:
+        _copy_prefix(out, src.buf[:rows_in], min(a, b), ctx)
     if layout.moved_rows() == 0:
         return out[:rows_out]
     tb = tables or pull_tables(layout, r, inverse, out.device)
-    src.epoch += 1
+    if phases & 1:
+        src.epoch += 1
     t = tb.table
     stream = int(torch.cuda.current_stream().cuda_stream)
     if copy_engine:
@@ -709,12 +884,11 @@ def remap_pull(layout: RemapLayout, src: PeerBuffer, out: torch.Tensor, ctx: Ran
                      h[0].ctypes.data, h[1].ctypes.data, h[2].ctypes.data, src.flag_ptrs.data_ptr(),
                      t[2].data_ptr(), t[3].data_ptr(), ctx.world, r, src.epoch, stream)
         return out[:rows_out]
-    ops._count_launch(3)
+    ops._count_launch(bin(phases).count("1"))
     with ctx.span("intra-comm", "remap.inverse" if inverse else "remap.forward", {"tokens": int(tb.host[2].sum())}):
-        _native.call("zp_remap_pull", out.data_ptr(), src.row_bytes, src.peer_ptrs.data_ptr(),
-                 t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), src.flag_ptrs.data_ptr(),
-                 t[3].data_ptr(), ctx.world, r, src.epoch, tb.max_count,
-                 int(torch.cuda.current_stream().cuda_stream))
+        _native.call("zp_remap_pull_phased", out.data_ptr(), src.row_bytes, src.peer_ptrs.data_ptr(),
+                     t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), src.flag_ptrs.data_ptr(),
+                     t[3].data_ptr(), ctx.world, r, src.epoch, tb.max_count, phases, stream)
     return out[:rows_out]
 
 
@@ -742,16 +916,16 @@ class ZeppelinLayer:
     def prepare(self, batch):
         self.plan = build_plan(batch, self.cluster)
         self.schedule = build_schedule(self.plan)
-        self.program = build_rank_program(self.plan, self.schedule, self.ctx.rank, self.n_heads)
+        # the reference's minimax transfer matrix for this cluster (remapping.py:187-245)
+        remap = solve_remap(self.plan.tokens_per_rank, cost_matrix(self.cluster))
+        self.program = build_rank_program(self.plan, self.schedule, self.ctx.rank, self.n_heads, remap)
         if not hasattr(self, "_stager"):
             self._stager = TableStager(self.ctx.device)
             self._remap_stager = TableStager(self.ctx.device)
         self.device_program = DeviceProgram(self.program, self.ctx.device, self._stager)
         self._pull = None
         if self.ctx.world > 1 and self.remap_method == "pull":
-            lay, r, dev = self.program.remap, self.ctx.rank, self.ctx.device
-            self._pull = (pull_tables(lay, r, False, dev, self._remap_stager),
-                          pull_tables(lay, r, True, dev, self._remap_stager))
+            self._pull = pull_table_pair(self.program.remap, self.ctx.rank, self._remap_stager)
         return self.plan
 
     @property
@@ -825,6 +999,7 @@ class ZeppelinLayer:
                 fw, inv = self._pull or (None, None)
                 remap_pull(self.layout, peer, act, ctx, tables=fw)
                 remap_pull(self.layout, peer, act, ctx, inverse=True, tables=inv)
+                self._remap_stager.release()  # both readers of this step's tables are enqueued
             else:
                 remap_push(self.layout, act[:rows], peer, ctx)
                 remap_push(self.layout, act[:self.layout.linear_rows[ctx.rank]], peer, ctx, inverse=True)

@@ -64,6 +64,51 @@ class RingProgram:
         """Rows arriving from prev_rank for round ``round_index + 1``."""
         return self.held_rows[ring_source(self.position, round_index + 1, self.group_size)]
 
+    @property
+    def n_buffers(self) -> int:
+        """KV buffers per rank: three for rings of 3+ members (a set waits only
+        for the round two rounds back to free its buffer), two otherwise."""
+        return 3 if self.group_size > 2 else 2
+
+    def hops(self) -> list["RingHop"]:
+        """The pull protocol of this position's g-1 hops (see RingHop)."""
+        g, nb = self.group_size, self.n_buffers
+        return [RingHop(round_index=r, src_buf=r % nb, dst_buf=(r + 1) % nb, rows=self.recv_rows(r),
+                        full=r, free=(r + 1 - nb) if r + 1 - nb >= 0 else None, consumed=r,
+                        next_full=(r + 1) if r + 1 <= g - 2 else None)
+                for r in range(g - 1)]
+
+
+@dataclass(frozen=True)
+class RingHop:
+    """Hop r of a ring position (reference attention_engine.py:247-251: after
+    round r the KV set held at position i-1 moves to position i), executed as
+    a pull by position i.  Epoch fields are offsets r' of the ring's epoch
+    base E: flags carry E + r'.
+
+    * wait until the predecessor announced ``full`` (its buffer ``src_buf``
+      holds the set for this position's round r+1);
+    * if ``free`` is set, wait until the successor announced it consumed hop
+      ``free`` from this rank (``dst_buf``'s previous content); the compute
+      stream also waits for round r+1-n_buffers, the buffer's last reader;
+    * copy ``rows`` KV rows predecessor[src_buf] -> own[dst_buf];
+    * announce ``consumed`` to the predecessor and, if ``next_full`` is set,
+      announce ``next_full`` to the successor (own ``dst_buf`` is what it
+      pulls at its hop r+1).
+
+    Position i's own set is packed into buffer 0 and announced to the
+    successor with epoch offset 0 before the first round.  A flag only grows:
+    a rank leaves a ring after its successor consumed its last hop, so no
+    epoch of a later ring can satisfy a wait of an earlier one."""
+    round_index: int
+    src_buf: int
+    dst_buf: int
+    rows: int
+    full: int
+    free: int | None
+    consumed: int
+    next_full: int | None
+
 
 @dataclass
 class RankProgram:

@@ -114,22 +114,3 @@ def route_schedule(schedule: AttentionSchedule, plan, cluster: ClusterSpec) -> d
                 if cluster.node_of(src) != cluster.node_of(dst) and n:
                     routes[(idx, r, src)] = build_route(cluster, ring, src, dst, n)
     return routes
-
-
-def ring_link_loads(schedule: AttentionSchedule, num_ranks: int) -> list[tuple[list[int], list[int]]]:
-    """Per ring round: KV tokens leaving / entering each GPU.  On NVSwitch the
-    bound is per-GPU egress/ingress; a ring puts at most one send and one
-    receive on each member per round."""
-    out = []
-    for rs in schedule.rings():
-        ring = rs.ring
-        g = ring.group_size
-        for r in range(g - 1):
-            tx = [0] * num_ranks
-            rx = [0] * num_ranks
-            for pos in range(g):
-                n = rs.rounds[pos][r].comm_tokens
-                tx[ring.members[pos]] += n
-                rx[ring.members[(pos + 1) % g]] += n
-            out.append((tx, rx))
-    return out

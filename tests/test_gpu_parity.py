@@ -110,3 +110,61 @@ def test_parity_mode_is_the_same_pipeline():
     torch.cuda.synchronize()
     assert (o_p - o_b.float()).abs().max().item() <= 1e-2
     assert (lse_p - lse_b).abs().max().item() <= 1e-4
+
+
+@pytest.mark.parametrize("g", [2, 4])
+def test_c3_ring_within_north_star_tolerance(g):
+    """Config 3 at full size (65,536 tokens per rank, one 131,072-token
+    sequence split over a ring): every rank's LocalTasks and ring rounds run
+    through the production ring executor (copy-engine KV pulls, triple
+    buffers, stream flags), all ranks emulated on one B200; each fragment's
+    rows are compared with the fp32 reference of its whole sequence."""
+    from paper_2509_21841_b200 import plan as P, schedule as S
+    from paper_2509_21841_b200.emulate import emulate_ranks_on_one_gpu
+    batch = W.c3_batch(g)
+    plan = P.build_plan(batch, W.cluster_for(batch, g))
+    sched = S.build_schedule(plan)
+    assert plan.ring_groups and max(plan.sequence_lengths.values()) == 131072
+    seqs = sorted(plan.sequence_lengths.items())
+    gen = torch.Generator(device="cuda").manual_seed(100 + g)
+    mk = lambda n, h: torch.randn(n, h, 128, device="cuda", generator=gen, dtype=torch.bfloat16)  # noqa: E731
+    sq = {s: mk(n, 32) for s, n in seqs}
+    sk = {s: mk(n, 8) for s, n in seqs}
+    sv = {s: mk(n, 8) for s, n in seqs}
+    outs_b = emulate_ranks_on_one_gpu(plan, sched, sq, sk, sv)
+    outs_p = emulate_ranks_on_one_gpu(plan, sched, sq, sk, sv, parity=True)
+    prod, par = ErrorStats(), ErrorStats()
+    spots = {}
+    for s, n in seqs:
+        ro, rl = causal_attention_fp32(sq[s], sk[s], sv[s])
+        for rank in range(plan.num_ranks):
+            r = 0
+            for f in plan.fragments[rank]:
+                if f.sequence_id == s:
+                    mine, rows = slice(r, r + f.tokens), slice(f.start, f.end)
+                    prod.add(outs_b[rank][0][mine], ro[rows], outs_b[rank][1][:, mine], rl[:, rows])
+                    par.add(outs_p[rank][0][mine], ro[rows], outs_p[rank][1][:, mine], rl[:, rows])
+                r += f.tokens
+        if n == 131072:
+            # fp64 spot rows of the ring sequence, looked up in the rank holding them
+            where = {}
+            for rank in range(plan.num_ranks):
+                r = 0
+                for f in plan.fragments[rank]:
+                    if f.sequence_id == s:
+                        where[(f.start, f.end)] = (rank, r)
+                    r += f.tokens
+            o_b = torch.empty(n, 32, 128, dtype=torch.bfloat16, device="cuda")
+            o_p = torch.empty(n, 32, 128, dtype=torch.float32, device="cuda")
+            for (a, b), (rank, r) in where.items():
+                o_b[a:b] = outs_b[rank][0][r:r + b - a]
+                o_p[a:b] = outs_p[rank][0][r:r + b - a]
+            spots = _spot_check(sq[s], sk[s], sv[s], ro, rl, [1, 65535, 65536, 98303, n - 1], o_b, o_p)
+        del ro, rl
+    _record(f"c3_g{g}", {"ring_groups": [list(rg.members) for rg in plan.ring_groups],
+                         "bf16": prod.as_dict(), "parity": par.as_dict(), "spot_rows_128k": spots})
+    assert prod.elements == sum(n for _, n in seqs) * 32 * 128
+    assert prod.max_abs <= MAX_ABS, prod.as_dict()
+    assert par.mean_rel <= MEAN_REL, par.as_dict()
+    assert par.max_abs <= MAX_ABS, par.as_dict()
+    assert prod.lse_max_abs <= LSE_ABS and par.lse_max_abs <= LSE_ABS

@@ -1,6 +1,8 @@
 """World-size-2 host path over gloo on CPU: ring KV exchange bookkeeping and
 the remap all-to-allv slices, with the kernel replaced by the oracle's
-work-item interpreter (test-only)."""
+work-item interpreter (test-only).  The ring hops follow the executor's pull
+plan (RingProgram.hops: buffer indices and row counts), with each pull of
+hop r carried by a gloo send/recv pair instead of a copy-engine read."""
 import os
 import socket
 
@@ -16,7 +18,6 @@ from oracle import worklist as OW
 from paper_2509_21841_b200 import plan as P, schedule as S, workloads as W
 from paper_2509_21841_b200.batch import SequenceBatch
 from paper_2509_21841_b200.cluster import ClusterSpec
-from paper_2509_21841_b200.engine import ring_p2p_ops
 from paper_2509_21841_b200.program import build_rank_program
 
 
@@ -45,18 +46,26 @@ def _worker(rank, world, port, lengths, cap, results):
         OW.run_items(pr.local.items, pr.local.segs, q, k, v, o, lse, None, d ** -0.5)
         for rp in pr.rings:
             rows = max(rp.held_rows)
-            bufs = [torch.zeros(rows, 2, hkv, d, dtype=torch.float64) for _ in range(2)]
+            nb = rp.n_buffers
+            hops = rp.hops()
+            bufs = [torch.zeros(rows, 2, hkv, d, dtype=torch.float64) for _ in range(nb)]
             for dst, src, cnt in rp.pack_ranges:
                 bufs[0][dst:dst + cnt, 0] = torch.from_numpy(k[src:src + cnt])
                 bufs[0][dst:dst + cnt, 1] = torch.from_numpy(v[src:src + cnt])
             st = OW.State(max(rp.state_rows, 1), hq, d)
             for r in range(rp.group_size):
-                cur, nxt = bufs[r % 2], bufs[(r + 1) % 2]
                 rr = rp.rounds[r]
-                kv = cur[:rr.kv_rows].numpy()
+                kv = bufs[r % nb][:rr.kv_rows].numpy()
                 OW.run_items(rr.work.items, rr.work.segs, q, kv[:, 0], kv[:, 1], o, lse, st, d ** -0.5)
                 if r < rp.group_size - 1:
-                    ops = ring_p2p_ops(rp, r, cur, nxt)
+                    h = hops[r]
+                    # successor pulls my src_buf (same index on every position); I pull the predecessor's
+                    ops = []
+                    if rp.send_rows(r):
+                        ops.append(dist.P2POp(dist.isend, bufs[h.src_buf][:rp.send_rows(r)].contiguous(),
+                                              rp.next_rank))
+                    if h.rows:
+                        ops.append(dist.P2POp(dist.irecv, bufs[h.dst_buf][:h.rows], rp.prev_rank))
                     if ops:
                         for req in dist.batch_isend_irecv(ops):
                             req.wait()
