@@ -327,6 +327,12 @@ def _ring_steps(ctx: RankContext, rp, epoch0: int, dev_pack, dev_rounds, q, k, v
     ops.copy_rows(bufs[0][:, 0], k, dev_pack, n_pack, max_pack)
     ops.copy_rows(bufs[0][:, 1], v, dev_pack, n_pack, max_pack)
     _native.call("zp_stream_write_flag", T.full_flag(succ, me), epoch0, int(cs.cuda_stream))
+    # this ring's hops start after the pack: they refill buffers the previous
+    # ring's rounds read, and their flag writes must land after the pack's
+    # (a flag only grows)
+    packed = torch.cuda.Event()
+    packed.record(cs)
+    xs.wait_event(packed)
     yield
     hops = rp.hops()
     ready: dict[int, torch.cuda.Event] = {}
@@ -337,8 +343,14 @@ def _ring_steps(ctx: RankContext, rp, epoch0: int, dev_pack, dev_rounds, q, k, v
             h = hops[r]
             if h.free is not None:
                 xs.wait_event(done[h.free])  # the dst buffer's last local reader
+            if ctx.tracer is not None:
+                # traced step: wait for the flags first, so the span times the copy alone
+                _native.call("zp_stream_wait_flag", T.full_flag(me, pred), epoch0 + h.full, int(xs.cuda_stream))
+                if h.free is not None:
+                    _native.call("zp_stream_wait_flag", T.consumed_flag(me, succ), epoch0 + h.free,
+                                 int(xs.cuda_stream))
             with ctx.span("intra-comm", "kv.send", {"ring": rp.ring_index, "round": r, "tokens": h.rows,
-                                                     "src": pred}, xs):
+                                                     "bytes": h.rows * T.row_bytes, "src": pred}, xs):
                 _native.call("zp_ring_hop", T.buf_addr(me, h.dst_buf), T.buf_addr(pred, h.src_buf),
                              h.rows * T.row_bytes, T.full_flag(me, pred), epoch0 + h.full,
                              T.consumed_flag(me, succ) if h.free is not None else None,

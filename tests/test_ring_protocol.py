@@ -34,6 +34,9 @@ class Flags:
 
     def write(self, owner, idx, val):
         with self.cv:
+            # a flag only grows (waits compare with >=): a smaller epoch landing
+            # after a larger one would strand its waiter
+            assert ((val - self.v[owner][idx]) & 0xFFFFFFFF) < 0x80000000, (owner, idx, self.v[owner][idx], val)
             self.v[owner][idx] = val
             self.cv.notify_all()
 
@@ -49,7 +52,10 @@ def _jitter(rng, scale):
     time.sleep(rng.random() * scale)
 
 
-def _run_rank(rank, progs, flags, bufs, errors, seed):
+ITERATIONS = 3
+
+
+def _run_rank(rank, progs, flags, bufs, errors, seed, n_rings):
     """Mirror of engine.attention_steps/_ring_steps for one rank: the comm
     thread runs the hops, the compute thread the pack and rounds; events
     are threading.Events (stream event edges)."""
@@ -60,54 +66,62 @@ def _run_rank(rank, progs, flags, bufs, errors, seed):
     world = flags.world
     epoch = 16
     try:
-        for rp in prog.rings:
-            e0 = epoch + 16 * rp.ring_index
-            g, me, pred, succ = rp.group_size, rank, rp.prev_rank, rp.next_rank
-            nb = rp.n_buffers
-            hops = rp.hops()
-            ready = {r: threading.Event() for r in range(1, g)}
-            done = {r: threading.Event() for r in range(g)}
-            comm_err = []
-
-            def comm():
-                try:
-                    for h in hops:
-                        if h.free is not None:
-                            assert done[h.free].wait(TIMEOUT), "local reader never finished"
-                        flags.wait(me, pred, e0 + h.full)
-                        if h.free is not None:
-                            flags.wait(me, world + succ, e0 + h.free)
-                        _jitter(rng, comm_scale)
-                        want = (rp.ring_index, (rp.position - 1 - h.round_index) % g)
-                        got = bufs[pred][h.src_buf]
-                        assert got == want, f"rank {me} hop {h.round_index}: pred buffer holds {got}, want {want}"
-                        bufs[me][h.dst_buf] = got
-                        flags.write(pred, world + me, e0 + h.consumed)
-                        if h.next_full is not None:
-                            flags.write(succ, me, e0 + h.next_full)
-                        ready[h.round_index + 1].set()
-                except BaseException as exc:  # noqa: BLE001
-                    comm_err.append(exc)
-
-            # compute stream: the previous ring's end wait happened below; pack
-            bufs[me][0] = (rp.ring_index, rp.position)
-            flags.write(succ, me, e0)
-            t = threading.Thread(target=comm)
-            t.start()
-            for r in range(g):
-                if r > 0:
-                    assert ready[r].wait(TIMEOUT), f"rank {me} ring {rp.ring_index}: set for round {r} never came"
-                _jitter(rng, compute_scale)
-                want = (rp.ring_index, ring_source(rp.position, r, g))
-                got = bufs[me][r % nb]
-                assert got == want, f"rank {me} round {r}: buffer holds {got}, want {want}"
-                done[r].set()
-            t.join(TIMEOUT)
-            if comm_err:
-                raise comm_err[0]
-            flags.wait(me, world + succ, e0 + g - 2)
+        for it in range(ITERATIONS):
+            _one_call(rank, prog, flags, bufs, rng, comm_scale, compute_scale, epoch + it * 16 * n_rings)
     except BaseException as exc:  # noqa: BLE001
         errors.append((rank, exc))
+
+
+def _one_call(rank, prog, flags, bufs, rng, comm_scale, compute_scale, epoch):
+    """One attention_forward: every ring of this rank in schedule order."""
+    world = flags.world
+    for rp in prog.rings:
+        e0 = epoch + 16 * rp.ring_index
+        g, me, pred, succ = rp.group_size, rank, rp.prev_rank, rp.next_rank
+        nb = rp.n_buffers
+        hops = rp.hops()
+        ready = {r: threading.Event() for r in range(1, g)}
+        done = {r: threading.Event() for r in range(g)}
+        comm_err = []
+
+        def comm():
+            try:
+                for h in hops:
+                    if h.free is not None:
+                        assert done[h.free].wait(TIMEOUT), "local reader never finished"
+                    flags.wait(me, pred, e0 + h.full)
+                    if h.free is not None:
+                        flags.wait(me, world + succ, e0 + h.free)
+                    _jitter(rng, comm_scale)
+                    want = (rp.ring_index, (rp.position - 1 - h.round_index) % g)
+                    got = bufs[pred][h.src_buf]
+                    assert got == want, f"rank {me} hop {h.round_index}: pred buffer holds {got}, want {want}"
+                    bufs[me][h.dst_buf] = got
+                    flags.write(pred, world + me, e0 + h.consumed)
+                    if h.next_full is not None:
+                        flags.write(succ, me, e0 + h.next_full)
+                    ready[h.round_index + 1].set()
+            except BaseException as exc:  # noqa: BLE001
+                comm_err.append(exc)
+
+        # compute stream: the previous ring's end wait happened below; pack,
+        # then the comm stream starts this ring's hops (event edge)
+        bufs[me][0] = (rp.ring_index, rp.position)
+        flags.write(succ, me, e0)
+        t = threading.Thread(target=comm)
+        t.start()
+        for r in range(g):
+            if r > 0:
+                assert ready[r].wait(TIMEOUT), f"rank {me} ring {rp.ring_index}: set for round {r} never came"
+            _jitter(rng, compute_scale)
+            want = (rp.ring_index, ring_source(rp.position, r, g))
+            got = bufs[me][r % nb]
+            assert got == want, f"rank {me} round {r}: buffer holds {got}, want {want}"
+            done[r].set()
+        t.join(TIMEOUT)
+        if comm_err:
+            raise comm_err[0]
+        flags.wait(me, world + succ, e0 + g - 2)
 
 
 @pytest.mark.parametrize("seed", range(16))
@@ -124,7 +138,8 @@ def test_pull_protocol_delivers_every_round_without_races(seed):
     flags = Flags(g)
     bufs = [[None] * 3 for _ in range(g)]
     errors = []
-    threads = [threading.Thread(target=_run_rank, args=(r, progs, flags, bufs, errors, seed)) for r in range(g)]
+    threads = [threading.Thread(target=_run_rank, args=(r, progs, flags, bufs, errors, seed,
+                                                                 len(sched.rings()))) for r in range(g)]
     for t in threads:
         t.start()
     for t in threads:
