@@ -12,8 +12,9 @@ layout -> inverse remap.  Prints ONE JSON line on rank 0.
          github<=128K sample (seed 1), split across GPUs by the planner; ring
          KV exchange over NVLink + remap all-to-allv.
 
-  --impl reference: the reference's CPU path (the oracle port: numpy fp32
-  attention + remap on the planner's plan) on the host cores, bounded sample.
+  --impl reference: the layer's CPU path on the host cores: the reference
+  package's own planner (baseline/_ref) + torch fp32 SDPA attention of every
+  sequence + the remap row moves, whole steps, no extrapolation.
 """
 
 from __future__ import annotations
@@ -248,11 +249,18 @@ def run_gpu(args):
         if world > 1:
             dist.destroy_process_group()
         return
-    traffic = None
-    prof_path = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    # DRAM bytes of this workload's attention launches (busiest rank, one step),
+    # measured by ncu for exactly this config (tools/traffic_capture.py)
+    traffic, traffic_note = None, "no ncu capture for this N in profiles/r02_attn_traffic.json"
+    prof_path = os.path.join(ROOT, "profiles", "r02_attn_traffic.json")
     if os.path.exists(prof_path):
         try:
-            traffic = json.load(open(prof_path)).get("bytes_per_launch")
+            cap = json.load(open(prof_path)).get(f"n{world}")
+            if cap:
+                traffic = cap["dram_bytes_per_step"]
+                traffic_note = (f"ncu dram__bytes_read+write of the {cap['launches']} attention launch(es) of one step "
+                                f"({cap['workload']}; algorithmic {cap['algorithmic_bytes_per_step']:.3e} B); "
+                                "cold-cache serialised capture")
         except Exception:
             traffic = None
     line = {
@@ -291,6 +299,7 @@ def run_gpu(args):
             "frac_of_sustained": ((achieved if world == 1 else per_rank[busiest][0]) / peak_sus) if peak_sus else None,
             "peak_kind": f"{peak_kind} burst bf16 (MEASURED_PEAKS.json)",
             "traffic": traffic,
+            "traffic_note": traffic_note,
             "kernel": "zp_attn_fwd (attn_fwd_kernel)",
             "flop_per_pair": FLOP_PER_PAIR,
             "rank": busiest,
@@ -304,7 +313,7 @@ def run_gpu(args):
         "e2e": e2e,
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(plan, sched, args.cpu_seconds)
+        line["cpu_baseline"] = cpu_baseline(batch, cluster, world)
     emit(line)
     if world > 1:
         dist.destroy_process_group()
@@ -436,86 +445,167 @@ def run_remap_stress(ctx, dev, world, rank, args, total=262144, iters=10):
 
 # ---------------------------------------------------------------------------- CPU arm
 
-def cpu_baseline(plan, sched, seconds: float):
-    """The oracle port (numpy fp32 attention; threads = all host cores) on a
-    bounded sample of the step's attention work, extrapolated by exact pairs."""
-    import numpy as np
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
-    from oracle import attention as OA
 
-    cores = os.cpu_count() or 1
-    rng = np.random.default_rng(0)
-    sizes = sorted(plan.sequence_lengths.items(), key=lambda kv: -kv[1])
-    total_pairs = sum(n * (n + 1) // 2 for _, n in sizes)
-    # sample: query rows of the longest sequence, growing until the time budget
-    sid, n = sizes[0]
-    hq, hkv, d = 32, 8, 128
-    k = rng.standard_normal((n, hkv, d), dtype=np.float32)
-    v = rng.standard_normal((n, hkv, d), dtype=np.float32)
-    done_pairs, spent, rows = 0, 0.0, 0
-    block = 256
-    while spent < seconds and rows < n:
-        if done_pairs:
-            # size the next block to the remaining budget (blocks double otherwise)
-            rate = spent / done_pairs
-            while block > 64 and rate * block * (rows + block / 2) > max(seconds - spent, 0.25 * seconds):
-                block //= 2
-        r1 = min(n, rows + block)
-        q = rng.standard_normal((r1 - rows, hq, d), dtype=np.float32)
+def _reference_package():
+    """The UNMODIFIED reference (varlenplan) installed into baseline/_ref
+    (pip install --target baseline/_ref /root/reference; travels to the GPU
+    box with the snapshot).  None when it is not installed: the bit-exact
+    restatement of its planner (paper_2509_21841_b200) is timed instead."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "varlenplan")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import varlenplan
+    return varlenplan
+
+
+class CpuLayer:
+    """The layer's CPU path, every rank's work in one process (BASELINE.md
+    section 2): the reference's own planner (build_plan + build_schedule +
+    solve_remap on the step's batch) and the CPU fp32 torch restatement of
+    the work it only counts — causal GQA attention of every sequence
+    (scaled_dot_product_attention, enable_gqa; whole sequences: the ring
+    rounds compose to exactly this) and the remap row moves (index_select
+    along the R3 permutation).  All host threads."""
+
+    def __init__(self, batch, cluster, world: int):
+        import numpy as np
+        import torch
+
+        from paper_2509_21841_b200 import plan as P, remap as M
+
+        torch.set_num_threads(os.cpu_count() or 1)
+        self.batch, self.cluster, self.world = batch, cluster, world
+        self.vp = _reference_package()
+        if self.vp is not None:
+            self.ref_batch = self.vp.SequenceBatch(tuple(batch.sequences))
+            c = cluster
+            self.ref_cluster = self.vp.ClusterSpec(c.num_nodes, c.gpus_per_node, c.token_capacity,
+                                                   c.inv_bw_intra, c.inv_bw_inter)
+        g = torch.Generator().manual_seed(0)
+        self.seqs = [(sid, n) for sid, n in sorted(batch.sequences, key=lambda x: -x[1])]
+        self.qkv = {sid: (torch.randn(1, 32, n, 128, generator=g), torch.randn(1, 8, n, 128, generator=g),
+                          torch.randn(1, 8, n, 128, generator=g)) for sid, n in self.seqs}
+        plan = P.build_plan(batch, cluster)
+        self.lay = M.remap_layout(plan.tokens_per_rank, M.solve_remap(plan.tokens_per_rank, M.cost_matrix(cluster)))
+        # remap payload: hidden 4096 fp32 rows per rank (attention layout), and
+        # the gather index of every linear-layout row (oracle rule R3)
+        from oracle import remap as OR
+        src = OR.source_map(list(self.lay.attn_rows), self.lay.matrix)
+        self.x = [torch.randn(n, 4096, generator=g) for n in self.lay.attn_rows] if world > 1 else []
+        self.gather = [(torch.from_numpy(np.ascontiguousarray(s[:, 0])), torch.from_numpy(np.ascontiguousarray(s[:, 1])))
+                       for s in src] if world > 1 else []
+        self.pairs = sum(n * (n + 1) // 2 for _, n in self.seqs)
+
+    def planner(self):
+        if self.vp is not None:
+            plan = self.vp.build_plan(self.ref_batch, self.ref_cluster)
+            self.vp.build_schedule(plan)
+            self.vp.solve_remap(list(plan.tokens_per_rank), self.vp.cost_matrix(self.ref_cluster))
+        else:
+            from paper_2509_21841_b200 import plan as P, remap as M, schedule as S
+            plan = P.build_plan(self.batch, self.cluster)
+            S.build_schedule(plan)
+            M.solve_remap(plan.tokens_per_rank, M.cost_matrix(self.cluster))
+
+    def step(self, limit_tokens: int | None = None) -> dict:
+        """One full step (or, for warm-up, attention of the first
+        ``limit_tokens`` rows of the shortest sequence).  Returns seconds per
+        phase."""
+        import torch
+        import torch.nn.functional as F
+
         t0 = time.perf_counter()
-        _, _, pairs = OA.causal_attention(q, k[:r1], v[:r1], np.arange(rows, r1), np.arange(r1), d ** -0.5,
-                                          dtype=np.float32)
-        spent += time.perf_counter() - t0
-        done_pairs += pairs
-        rows = r1
-        block = min(block * 2, 4096)
-    est = spent * total_pairs / max(done_pairs, 1)
-    total_tokens = sum(x for _, x in sizes)
-    return {"value": total_tokens / est, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"oracle numpy fp32 causal attention, query rows [0,{rows}) of the {n}-token sequence "
-                      f"({done_pairs} of {total_pairs} pairs, {spent:.1f} s), extrapolated by exact pair count; "
-                      f"remap is a no-op at N=1 and the planner (<1 ms) is excluded"}
+        self.planner()
+        t1 = time.perf_counter()
+        with torch.no_grad():
+            for sid, n in (self.seqs if limit_tokens is None else self.seqs[-1:]):
+                q, k, v = self.qkv[sid]
+                if limit_tokens is not None:
+                    m = min(n, limit_tokens)
+                    q, k, v = q[:, :, :m], k[:, :, :m], v[:, :, :m]
+                F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
+        t2 = time.perf_counter()
+        if limit_tokens is None:
+            for j in range(self.world if self.x else 0):
+                ranks, rows = self.gather[j]
+                out = torch.empty(len(rows), 4096)
+                for r in range(self.world):
+                    sel = (ranks == r).nonzero().squeeze(1)
+                    if sel.numel():
+                        out.index_copy_(0, sel, self.x[r].index_select(0, rows[sel].long()))
+        t3 = time.perf_counter()
+        return {"planner_s": t1 - t0, "attention_s": t2 - t1, "remap_s": t3 - t2, "total_s": t3 - t0}
+
+    def describe(self, kind: str) -> str:
+        planner = ("the reference package itself (varlenplan from baseline/_ref): build_plan + build_schedule + "
+                   "solve_remap" if self.vp is not None else
+                   "the bit-exact planner restatement (reference not installed): build_plan + build_schedule + "
+                   "solve_remap")
+        return (f"whole {self.batch.total_tokens}-token batch every step, no extrapolation: {planner}; "
+                f"torch fp32 scaled_dot_product_attention(is_causal, enable_gqa) over all {len(self.seqs)} "
+                f"sequences ({self.pairs} causal pairs x 32 heads)"
+                + ("; remap index_select fwd over all ranks" if self.x else "; remap is a no-op at N=1")
+                + f"; {os.cpu_count()} threads on {_cpu_model()}")
+
+
+def cpu_baseline(batch, cluster, world: int):
+    """cpu_baseline field of the GPU arm's line (rank 0, N=1): one full step
+    of the CPU path after a short warm-up."""
+    cl = CpuLayer(batch, cluster, world)
+    cl.step(limit_tokens=512)
+    st = cl.step()
+    return {"value": batch.total_tokens / st["total_s"], "unit": UNIT, "cores": os.cpu_count() or 1,
+            "kind": "port", "sample": cl.describe("baseline"),
+            "phases_s": st, "cpu_model": _cpu_model(),
+            "attention_tflops": cl.pairs * FLOP_PER_PAIR / st["attention_s"] / 1e12}
 
 
 def run_reference(args):
+    """--impl reference: the CPU path of the same metric and config on the
+    host cores (rank 0 only).  Warm-up steps run the planner plus a short
+    attention slice; timed steps are whole steps (no extrapolation), at
+    least 3 and then as many of the K requested as fit in --ref-budget
+    seconds; the value is the median."""
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    import numpy as np
-
-    from oracle import remap as OR
-    from paper_2509_21841_b200 import plan as P, remap as M, schedule as S
-
     name, batch, cluster = workload(args.gpus)
-    plan = P.build_plan(batch, cluster)
-    sched = S.build_schedule(plan)
-    per_step = max(3.0, min(30.0, 100.0 / max(1, args.steps + args.warmup)))
-    vals = []
-    for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(plan, sched, per_step)
-        if i >= args.warmup:
-            vals.append(cb["value"])
-    # the remap's CPU cost (numpy row moves) is added for N > 1
-    remap_note = ""
-    if args.gpus > 1:
-        lay = M.remap_layout(plan.tokens_per_rank)
-        xs = [np.zeros((n, 4096), dtype=np.float16) for n in plan.tokens_per_rank]
-        t0 = time.perf_counter()
-        y = OR.forward(xs, lay.matrix)
-        OR.inverse(y, lay.matrix, list(plan.tokens_per_rank))
-        remap_s = time.perf_counter() - t0
-        vals = [batch.total_tokens / (batch.total_tokens / v + remap_s) for v in vals]
-        remap_note = f"; + numpy remap fwd/inv of all ranks ({remap_s * 1e3:.0f} ms)"
-    value = statistics.median(vals)
-    ms = batch.total_tokens / value * 1e3
+    cl = CpuLayer(batch, cluster, args.gpus)
+    for _ in range(args.warmup):
+        cl.step(limit_tokens=512)
+    steps = []
+    t_start = time.perf_counter()
+    for i in range(args.steps):
+        steps.append(cl.step())
+        if len(steps) >= 3 and time.perf_counter() - t_start > args.ref_budget:
+            break
+    med = statistics.median(s["total_s"] for s in steps)
+    value = batch.total_tokens / med
+    phases = {k: statistics.median(s[k] for s in steps) for k in steps[0]}
     emit({
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-        "config": {"workload": name, "total_tokens": batch.total_tokens},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb["cores"], "kind": "port",
-                         "sample": cb["sample"] + remap_note},
+        "warmup": args.warmup, "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (same batch as the GPU arm; N(0,1) fp32 q/k/v)",
+        "impl": "reference",
+        "config": {"workload": name, "total_tokens": batch.total_tokens, "sequences": len(batch)},
+        "steps_timed": len(steps), "phases_s_median": phases,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count() or 1,
+                         "kind": "port", "sample": cl.describe("reference"),
+                         "cpu_model": _cpu_model(),
+                         "attention_tflops": cl.pairs * FLOP_PER_PAIR / phases["attention_s"] / 1e12},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     })
 
@@ -785,7 +875,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["zeppelin", "reference"], default="zeppelin")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-budget", type=float, default=240.0,
+                    help="--impl reference: stop timing whole steps after this many seconds (>= 3 steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-remap-stress", action="store_true")

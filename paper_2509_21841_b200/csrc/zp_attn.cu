@@ -52,7 +52,10 @@ constexpr int kSchedSlots = 4;
 #define ZP_MMA_UNROLL 8
 #endif
 #ifndef ZP_WG0_REGS
-#define ZP_WG0_REGS 88  // producer / MMA warpgroup; the softmax warpgroups get 208
+#define ZP_WG0_REGS 88  // producer / MMA warpgroup
+#endif
+#ifndef ZP_SM_REGS
+#define ZP_SM_REGS 208  // each softmax warpgroup (thread = one 128-column S row)
 #endif
 constexpr int kMmaUnroll = ZP_MMA_UNROLL;
 
@@ -73,7 +76,7 @@ __device__ unsigned long long g_zp_trace[8192];  // CTA 0 at [0, 4096), CTA 1 at
   do {                 \
   } while (0)
 #endif
-static_assert(ZP_WG0_REGS * 128 + 208 * 256 <= 168 * 384, "setmaxnreg exceeds the launch register pool");
+static_assert(ZP_WG0_REGS * 128 + ZP_SM_REGS * 256 <= 168 * 384, "setmaxnreg exceeds the launch register pool");
 
 template <bool kPair>
 struct Cfg {
@@ -528,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(ZP_SM_REGS));
     // ---------------- softmax / correction / epilogue (thread == row)
     const int t = (warp - 4) >> 2;
     const int quad = warp & 3;

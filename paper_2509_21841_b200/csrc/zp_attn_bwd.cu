@@ -587,12 +587,14 @@ extern "C" int zp_attn_bwd(const void* q, const void* k, const void* v, const vo
   if ((rc = zp_make_tmap_2d_f32(&tdq, dq, uint64_t(hq) * kD, uint64_t(q_rows), uint64_t(hq) * kD * 4, 32, kBQ)) !=
       ZP_OK)
     return rc;
-  static bool attr_done = false;
-  if (!attr_done) {
+  static bool attr_done[64] = {};  // per device: the attribute is per device and function
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return zp_fail(ZP_ENODEV, "zp_attn_bwd: device");
+  if (!attr_done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(kSmemBytes));
     if (e != cudaSuccess) return zp_fail_cuda(e, "zp_attn_bwd: smem attribute");
-    attr_done = true;
+    attr_done[dev] = true;
   }
   BwdArgs a;
   a.items = items;

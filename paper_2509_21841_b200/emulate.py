@@ -34,13 +34,21 @@ def gather_rank(seq_tensors: dict, plan, rank: int, device) -> torch.Tensor:
     return torch.cat(parts, 0).to(device).contiguous()
 
 
-def emulate_ranks_on_one_gpu(plan, sched, sq: dict, sk: dict, sv: dict, device="cuda", parity: bool = False):
+def emulate_ranks_on_one_gpu(plan, sched, sq: dict, sk: dict, sv: dict, device="cuda", parity: bool = False,
+                             softmax_scale: float | None = None):
     """Every rank's attention_forward on one GPU.  Returns [(o, lse)] per rank
     in attention layout (o bf16; fp32 with ``parity``: V converted to fp16 and
     the parity kernel, zp_attn_fwd_parity)."""
     hq = next(iter(sq.values())).shape[1]
     hkv, d = next(iter(sk.values())).shape[1:]
-    scale = 1.0 / math.sqrt(d)
+    ad = ops.HeadAdapter(hq, hkv, d)
+    if not ad.identity:  # e.g. config 1's 4 heads x d64 (MHA): padded / head-duplicated layout
+        adapted = {s: ad.inputs(sq[s], sk[s], sv[s]) for s in sq}
+        outs = emulate_ranks_on_one_gpu(plan, sched, {s: a[0] for s, a in adapted.items()},
+                                        {s: a[1] for s, a in adapted.items()}, {s: a[2] for s, a in adapted.items()},
+                                        device, parity, softmax_scale=d ** -0.5)
+        return [ad.outputs(o, lse) for o, lse in outs]
+    scale = 1.0 / math.sqrt(d) if softmax_scale is None else softmax_scale
     dev = torch.device(device)
     world = plan.num_ranks
     ctxs = [RankContext(r, world, dev) for r in range(world)]

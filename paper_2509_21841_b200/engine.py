@@ -1,11 +1,13 @@
 """Device executor: runs a rank's program (``program.py``) on its B200.
 
-One process per GPU.  Compute goes to the caller's current CUDA stream; ring
-KV exchange goes to a dedicated communication stream (NCCL point-to-point via
-``torch.distributed``), double-buffered so round r's attention overlaps the
-transfer of round r+1's KV set.  Rings run in ``schedule.rings()`` order on
-every rank, so rings that share ranks are entered in the same order
-everywhere (deadlock-free); a rank never waits on a ring it is not in.
+One process per GPU.  Compute goes to the caller's current CUDA stream; the
+ring KV exchange goes to a dedicated communication stream as copy-engine pulls
+from the predecessor's CUDA-IPC-mapped buffer, ordered by epoch flags that the
+stream front-end waits on (``RingTransport``, ``zp_ring_hop``: no SM, no
+collective library), triple-buffered so round r's attention overlaps the
+transfer of the next sets.  Rings run in ``schedule.rings()`` order on every
+rank, so rings that share ranks are entered in the same order everywhere
+(deadlock-free); a rank never waits on a ring it is not in.
 
 Public entry points (drop-in execution of what the reference only costs):
 
@@ -444,6 +446,19 @@ def attention_forward(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torch
     fp32 o; ``zp_attn_fwd_parity``).  Collective when the plan has rings:
     every rank of the context calls it with the same plan."""
     ctx = ctx or RankContext.from_env()
+    ad = ops.HeadAdapter(q.shape[1], k.shape[1], q.shape[2])
+    if not ad.identity:
+        # other head shapes (e.g. BASELINE config 1: 4 heads x d64, MHA) run on
+        # the padded / head-duplicated layout the kernel supports
+        scale = 1.0 / math.sqrt(q.shape[2]) if softmax_scale is None else softmax_scale
+        o2, lse2 = attention_forward(plan, schedule, *ad.inputs(q, k, v), ctx=ctx, softmax_scale=scale,
+                                     kv_exchange=kv_exchange)
+        o, lse = ad.outputs(o2, lse2)
+        if out is not None:
+            out[0].copy_(o)
+            out[1][:, :lse.shape[1]].copy_(lse)
+            return out
+        return o, lse
     hq = q.shape[1]
     prog = program or build_rank_program(plan, schedule, ctx.rank, hq)
     if q.shape[0] != prog.rows or k.shape[0] != prog.rows:

@@ -210,12 +210,55 @@ def local_fragments(seqlens: list[int] | np.ndarray, row0: int = 0) -> list[Quer
     return frags
 
 
+class HeadAdapter:
+    """Maps any attention head shape onto the kernel's (head_dim 128, even
+    GQA group): head_dim d < 128 is zero-padded (q.k and the softmax are
+    unchanged with the scale kept at 1/sqrt(d); the padded output columns are
+    exact zeros and dropped), and an odd group (MHA: hq == hkv) is made even
+    by running every query head twice against its KV head (outputs of the
+    copies are identical; one is kept).  BASELINE config 1 (4 heads x d64,
+    MHA) runs through this."""
+
+    def __init__(self, hq: int, hkv: int, d: int):
+        if d > HEAD_DIM or hq % hkv:
+            raise ValueError(f"unsupported head shape: hq={hq} hkv={hkv} head_dim={d} (need d <= 128, hkv | hq)")
+        self.hq, self.hkv, self.d = hq, hkv, d
+        self.dup = 2 if (hq // hkv) % 2 else 1
+
+    @property
+    def identity(self) -> bool:
+        return self.d == HEAD_DIM and self.dup == 1
+
+    @property
+    def kernel_heads(self) -> int:
+        return self.hq * self.dup
+
+    def inputs(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor):
+        pad = HEAD_DIM - self.d
+        if pad:
+            q, k, v = (torch.nn.functional.pad(x, (0, pad)) for x in (q, k, v))
+        if self.dup > 1:
+            q = q.repeat_interleave(self.dup, dim=1)
+        return q.contiguous(), k.contiguous(), v.contiguous()
+
+    def outputs(self, o: torch.Tensor, lse: torch.Tensor):
+        if self.dup > 1:
+            o, lse = o[:, ::self.dup], lse[::self.dup]
+        return o[..., :self.d].contiguous(), lse.contiguous()
+
+
 def varlen_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seqlens,
                      softmax_scale: float | None = None) -> tuple[torch.Tensor, torch.Tensor]:
     """Causal attention of packed variable-length sequences (all GPU-local):
-    the LocalTask queue of one rank.  Returns (o bf16 [T,Hq,128], lse fp32 [Hq,T]);
-    with an fp16 v the parity mode runs and o is fp32."""
+    the LocalTask queue of one rank.  Returns (o bf16 [T,Hq,d], lse fp32 [Hq,T]);
+    with an fp16 v the parity mode runs and o is fp32.  Any head_dim <= 128
+    and any GQA group (HeadAdapter)."""
     _require_cuda(q, k, v)
+    ad = HeadAdapter(q.shape[1], k.shape[1], q.shape[2])
+    if not ad.identity:
+        scale = 1.0 / math.sqrt(q.shape[2]) if softmax_scale is None else softmax_scale
+        o, lse = varlen_attention(*ad.inputs(q, k, v), seqlens, softmax_scale=scale)
+        return ad.outputs(o, lse)
     t, hq, _ = q.shape
     hkv = k.shape[1]
     wl = build_worklist(local_fragments(seqlens), hq // 2)

@@ -184,3 +184,26 @@ def test_single_cta_kernel_gqa_group_of_two():
         assert (o[r:r + n].float() - ro).abs().max().item() <= MAX_ABS
         assert (lse[:, r:r + n] - rl).abs().max().item() <= 1e-2
         r += n
+
+
+@pytest.mark.parametrize("hq,hkv,d", [(4, 4, 64), (4, 2, 64), (6, 2, 128), (8, 8, 96), (32, 8, 64)])
+def test_other_head_shapes_through_the_adapter(hq, hkv, d):
+    """BASELINE config 1's heads (4 x d64, MHA) and other shapes the kernel
+    does not take natively run through ops.HeadAdapter (zero-padded head_dim,
+    query heads duplicated for odd GQA groups), against fp32 with scale 1/sqrt(d)."""
+    seqlens = [306, 66, 1, 241]
+    t = sum(seqlens)
+    g = torch.Generator().manual_seed(hq * 100 + d)
+    q = torch.randn(t, hq, d, generator=g).to(torch.bfloat16).cuda()
+    k = torch.randn(t, hkv, d, generator=g).to(torch.bfloat16).cuda()
+    v = torch.randn(t, hkv, d, generator=g).to(torch.bfloat16).cuda()
+    o, lse = ops.varlen_attention(q, k, v, seqlens)
+    torch.cuda.synchronize()
+    assert o.shape == q.shape and lse.shape == (hq, t)
+    r = 0
+    for n in seqlens:
+        pos = torch.arange(n, device="cuda")
+        ro, rl = ref_attention(q[r:r + n], k[r:r + n], v[r:r + n], pos, pos)
+        assert (o[r:r + n].float() - ro).abs().max().item() <= MAX_ABS
+        assert (lse[:, r:r + n] - rl).abs().max().item() <= 1e-2
+        r += n

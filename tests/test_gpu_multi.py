@@ -244,3 +244,57 @@ def test_multi_gpu_backward_with_ring_dkv_exchange():
     assert any(v[1] > 0 for v in res.values()), "config must exercise rings"
     for rank, (rel, _) in res.items():
         assert rel <= 2.5e-2, res
+
+
+def _host_fed_worker(rank, world, port, results):
+    """ZeppelinLayer.step_host (pinned host inputs, per-step planning with the
+    work lists and both remap tables staged through reused slots, H2D / D2H
+    streams) over back-to-back steps with DIFFERENT batches: every step's
+    output equals the device path for that batch (no staged table or slot is
+    overwritten while a step that reads it is in flight)."""
+    import torch.distributed as dist
+    from paper_2509_21841_b200 import engine
+    from paper_2509_21841_b200.batch import SequenceBatch
+    from paper_2509_21841_b200.cluster import single_box
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        lens = [[3000, 300, 1200, 40, 700], [700, 40, 1200, 300, 3000], [2000, 2000, 1000, 200, 40],
+                [5000, 100, 80, 40, 20], [1240, 1000, 1000, 1000, 1000]]
+        batches = [SequenceBatch(tuple(enumerate(x))) for x in lens]
+        cluster = single_box(world, batches[0].total_tokens)
+        ctx = engine.RankContext(rank, world)
+        layer = engine.ZeppelinLayer(cluster, ctx)
+        g = torch.Generator().manual_seed(rank)
+        ins, outs = [], []
+        for b in batches:
+            layer.prepare(b)
+            rows = layer.program.rows
+            qkv = tuple(torch.randn(rows, h, 128, generator=g).to(torch.bfloat16).pin_memory() for h in (32, 8, 8))
+            ins.append(qkv)
+            outs.append(torch.empty(rows, 32, 128, dtype=torch.bfloat16).pin_memory())
+        for i, b in enumerate(batches):
+            layer.prepare(b)
+            layer.step_host(*ins[i], outs[i])
+        torch.cuda.synchronize()
+        ok = True
+        for i, b in enumerate(batches):
+            layer.prepare(b)
+            o, _ = layer.attention(*(x.cuda() for x in ins[i]))
+            torch.cuda.synchronize()
+            ok &= bool(torch.equal(outs[i], o.cpu()))
+        results[rank] = ok
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_host_fed_steps_with_varying_batches():
+    world = min(torch.cuda.device_count(), 4)
+    with mp.Manager() as mgr:
+        res = mgr.dict()
+        mp.spawn(_host_fed_worker, args=(world, _port(), res), nprocs=world, join=True)
+        res = dict(res)
+    assert sorted(res) == list(range(world)) and all(res.values()), res

@@ -23,12 +23,12 @@ def inputs(plan, seed, hq=32, hkv=8, d=128):
     return sq, sk, sv
 
 
-def check(plan, seed=0):
+def check(plan, seed=0, hq=32, hkv=8, d=128):
     sched = S.build_schedule(plan)
-    sq, sk, sv = inputs(plan, seed)
+    sq, sk, sv = inputs(plan, seed, hq, hkv, d)
     outs = emulate_ranks_on_one_gpu(plan, sched, sq, sk, sv)
     f64 = lambda m: {s: t.double().numpy() for s, t in m.items()}  # noqa: E731
-    ref, pairs = OA.run_plan(plan, sched, f64(sq), f64(sk), f64(sv), 128 ** -0.5)
+    ref, pairs = OA.run_plan(plan, sched, f64(sq), f64(sk), f64(sv), d ** -0.5)
     for (ri, i, r), cnt in pairs.items():
         assert cnt == sched.rings()[ri].rounds[i][r].compute_pairs
     worst = 0.0
@@ -44,6 +44,12 @@ def check(plan, seed=0):
 
 def test_c1_plan_llama_heads():
     check(P.build_plan(W.c1_batch(), W.c1_cluster()))
+
+
+def test_c1_at_its_own_shape():
+    """BASELINE config 1 exactly: the C1 plan (2 ranks, one ring) with 4 heads
+    x d64 MHA (through ops.HeadAdapter) against the fp64 oracle."""
+    check(P.build_plan(W.c1_batch(), W.c1_cluster()), hq=4, hkv=4, d=64)
 
 
 @pytest.mark.parametrize("g,lengths", [
