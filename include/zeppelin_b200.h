@@ -157,6 +157,12 @@ ZP_API int zp_copy_rows(void* dst, int64_t dst_stride_bytes, const void* src, in
                  int64_t row_bytes, const int32_t* ranges, int n_ranges, int max_rows_per_range,
                  void* stream);
 
+/* dst[i] += src[i] for n fp32 values (n % 4 == 0, 16-byte aligned): the ring
+ * backward adds the dK/dV partial sum received for a travelling KV set to this
+ * position's contribution before forwarding it (README.md:119-124 charges
+ * the g sends of a ring). */
+ZP_API int zp_add_f32(float* dst, const float* src, int64_t n, void* stream);
+
 /* Fused remap push (collective: every rank calls it with the same epoch).
  * flags_ptrs[r] points at rank r's int32[2*world] flag block (IPC-mapped):
  * [0,world) "done from sender s", [world,2*world) "ready from rank s".

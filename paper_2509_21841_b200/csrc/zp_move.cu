@@ -51,6 +51,22 @@ __global__ void __launch_bounds__(kMoveThreads)
   }
 }
 
+// dst[i] += src[i] (fp32, 16-byte vectors): the ring backward's running dK/dV
+// partial sum of a travelling KV set (received total + this position's share).
+__global__ void __launch_bounds__(kMoveThreads)
+    add_f32_kernel(float4* __restrict__ dst, const float4* __restrict__ src, int64_t n_vec) {
+  const int64_t step = int64_t(gridDim.x) * kMoveThreads;
+  for (int64_t i = int64_t(blockIdx.x) * kMoveThreads + threadIdx.x; i < n_vec; i += step) {
+    float4 a = dst[i];
+    const float4 b = __ldg(src + i);
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+    dst[i] = a;
+  }
+}
+
 // grid.y = destination rank; peer stores (st.global on IPC-mapped pointers).
 __global__ void __launch_bounds__(kMoveThreads)
     remap_push_kernel(const uint8_t* __restrict__ src, int64_t row_bytes,
@@ -188,6 +204,21 @@ static int grid_for(int64_t vecs, int per_y) {
   if (blocks < 1) blocks = 1;
   const int64_t cap = 148 * 8 / (per_y > 0 ? per_y : 1) + 1;
   return int(blocks < cap ? blocks : cap);
+}
+
+extern "C" int zp_add_f32(float* dst, const float* src, int64_t n, void* stream) {
+  if (n == 0) return ZP_OK;
+  if (n < 0 || (n & 3) || !dst || !src || ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15u))
+    return zp_fail(ZP_EINVAL, "zp_add_f32: need 16-byte aligned pointers and n % 4 == 0");
+  if (zp_check_device() != ZP_OK) return ZP_ENODEV;
+  const int64_t n_vec = n / 4;
+  int64_t blocks = (n_vec + zp::kMoveThreads - 1) / zp::kMoveThreads;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  zp::add_f32_kernel<<<int(blocks), zp::kMoveThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<float4*>(dst), reinterpret_cast<const float4*>(src), n_vec);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_add_f32: launch");
+  return ZP_OK;
 }
 
 extern "C" int zp_copy_rows(void* dst, int64_t dst_stride_bytes, const void* src,

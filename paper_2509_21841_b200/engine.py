@@ -419,19 +419,33 @@ def attention_steps(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torch.T
     """Generator form of ``attention_forward``: yields ``(ring_index, step)``
     after each ring step (pack = step 0, round r = step r+1).  Rings run in
     ``schedule.rings()`` order on every rank (reference attention_engine.py:
-    266-271), each position pulling the next KV set while it computes."""
+    266-271), each position pulling the next KV set while it computes; local
+    tasks fill the waits the reference's executor model predicts before each
+    ring and the rest run after the last ring (program.local_fill_plan)."""
     epoch = ctx.ring_epoch
     ctx.ring_epoch += 16 * len(schedule.rings())  # the same on every rank
-    if devp.local.n:
-        with ctx.span("compute", "local.attn", {"pairs": prog.local.pairs_per_head, "items": devp.local.n}):
-            ops.attn_fwd(q, k, v, devp.local.items, devp.local.n, devp.local.segs, o, lse, softmax_scale=scale)
-    for rp, (pack, rounds) in zip(prog.rings, devp.rings):
+    done = 0
+
+    def local_items(upto: int):
+        # LocalTask items [done, upto) of the longest-first list (zp_attn_fwd)
+        nonlocal done
+        if upto > done:
+            w = devp.local
+            with ctx.span("compute", "local.attn", {"items": upto - done}):
+                ops.attn_fwd(q, k, v, w.items[8 * done:8 * upto], upto - done, w.segs, o, lse, softmax_scale=scale)
+            done = upto
+
+    for j, (rp, (pack, rounds)) in enumerate(zip(prog.rings, devp.rings)):
+        # local work that fills this rank's predicted wait for the ring's
+        # slowest member (program.local_fill_plan), then the ring
+        local_items(prog.local_cuts[j] if j < len(prog.local_cuts) else done)
         if kv_exchange == "allgather":
             _run_ring_allgather(ctx, rp, pack, rounds, q, k, v, o, lse, scale)
             continue
         for step, _ in enumerate(_ring_steps(ctx, rp, epoch + 16 * rp.ring_index, pack, rounds, q, k, v, o,
                                              lse, scale)):
             yield rp.ring_index, step
+    local_items(devp.local.n)  # what is left runs after the last ring (simulator.py:181-187)
 
 
 def attention_forward(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
@@ -574,8 +588,8 @@ def _run_ring_backward(ctx: RankContext, rp, dev_pack, dev_rounds, dev_unpack, q
                                                "dst": rp.next_rank}, xs):
             xs.wait_event(done)
             if r > 0 and n_send:
-                zk[cur][:n_send].add_(ak[cur][:n_send])
-                zv[cur][:n_send].add_(av[cur][:n_send])
+                ops.add_f32_(zk[cur][:n_send], ak[cur][:n_send])
+                ops.add_f32_(zv[cur][:n_send], av[cur][:n_send])
             p2p = []
             if n_send:
                 p2p += [dist.P2POp(dist.isend, zk[cur][:n_send], rp.next_rank, ctx.group),

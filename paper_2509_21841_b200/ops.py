@@ -282,6 +282,17 @@ def copy_rows(dst: torch.Tensor, src: torch.Tensor, ranges: torch.Tensor, n_rang
                  max_rows, _stream_ptr(stream))
 
 
+def add_f32_(dst: torch.Tensor, src: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
+    """dst += src (contiguous fp32 of equal size), zp_add_f32."""
+    _require_cuda(dst, src)
+    if dst.dtype != torch.float32 or src.dtype != torch.float32 or dst.numel() != src.numel():
+        raise ValueError("add_f32_: fp32 tensors of equal size")
+    if not (dst.is_contiguous() and src.is_contiguous()):
+        raise ValueError("add_f32_: contiguous tensors")
+    _count_launch()
+    _native.call("zp_add_f32", dst.data_ptr(), src.data_ptr(), dst.numel(), _stream_ptr(stream))
+
+
 # ---------------------------------------------------------------- block kernels
 
 def rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float = 1e-5, out: torch.Tensor | None = None) -> torch.Tensor:

@@ -121,6 +121,9 @@ class RankProgram:
     remap: RemapLayout
     n_head_pairs: int
     local_frags: list[QueryFragment] = field(default_factory=list)
+    # local items [cuts[j-1], cuts[j]) run right before the j-th ring of this
+    # rank (cuts[-1] before the first); the rest after the last ring
+    local_cuts: list[int] = field(default_factory=list)
 
     @property
     def max_held_rows(self) -> int:
@@ -149,6 +152,40 @@ def _ring_buffer_rows(ring_sched: RingSchedule) -> list[dict[tuple[int, int], in
     return out
 
 
+def local_fill_plan(schedule: AttentionSchedule, num_ranks: int) -> dict[int, list[int]]:
+    """Local work (visible pairs per head) each rank runs before each of its
+    rings, so that LocalTasks fill the time a rank would otherwise wait for a
+    ring's slowest member.
+
+    The reference's executor model (simulator.py:136-187): rings run in
+    schedule order, a ring starts when all its members are ready (:139), local
+    tasks run after the rings (:181-187).  Here the same list schedule is
+    played with exact pair counts as the cost: at each ring, a member that
+    would be idle until the ring's start runs that much of its local work
+    first (longest tiles first); whatever local work is left runs after its
+    last ring.  Pure function of the schedule, so every rank derives the same
+    plan.  Returns rank -> [pairs before its 1st ring, before its 2nd, ...]."""
+    in_ring = {s.sequence_id for rs in schedule.rings() for s in rs.ring.sequences}
+    local_left = [0] * num_ranks
+    for t in schedule.local_tasks:
+        if t.sequence_id not in in_ring:
+            local_left[t.rank] += t.compute_pairs
+    ready = [0] * num_ranks
+    fill: dict[int, list[int]] = {r: [] for r in range(num_ranks)}
+    for rs in schedule.rings():
+        members = rs.ring.members
+        start = max(ready[m] for m in members)
+        for m in members:
+            take = min(start - ready[m], local_left[m])
+            fill[m].append(take)
+            local_left[m] -= take
+        work = [sum(rd.compute_pairs for rd in rs.rounds[i]) for i in range(len(members))]
+        end = start + max(work)
+        for m in members:
+            ready[m] = end
+    return fill
+
+
 def build_rank_program(plan, schedule: AttentionSchedule, rank: int, n_heads: int,
                        remap=None) -> RankProgram:
     n_hp = n_heads // 2
@@ -165,6 +202,11 @@ def build_rank_program(plan, schedule: AttentionSchedule, rank: int, n_heads: in
             local_frags.append(QueryFragment(row0=at, pos0=0, length=f.tokens, segs=[(at, 0, f.tokens)]))
         at += f.tokens
     local = build_worklist(local_frags, n_hp)
+    # local items run before each ring (cumulative cut points in the LPT list)
+    cuts, acc = [], 0
+    for take in local_fill_plan(schedule, plan.num_ranks)[rank]:
+        acc += take
+        cuts.append(local.cut(acc))
     want = sum(t.compute_pairs for t in schedule.local_tasks if t.rank == rank and t.sequence_id not in in_ring)
     if local.pairs_per_head != want:
         raise AssertionError(f"rank {rank}: local work list covers {local.pairs_per_head} pairs, schedule says {want}")
@@ -228,7 +270,7 @@ def build_rank_program(plan, schedule: AttentionSchedule, rank: int, n_heads: in
     elif not isinstance(remap, RemapLayout):
         remap = remap_layout(plan.tokens_per_rank, remap)
     return RankProgram(rank=rank, world=plan.num_ranks, rows=at, frag_rows=frag_rows, local=local,
-                       rings=rings, remap=remap, n_head_pairs=n_hp, local_frags=local_frags)
+                       rings=rings, remap=remap, n_head_pairs=n_hp, local_frags=local_frags, local_cuts=cuts)
 
 
 @dataclass

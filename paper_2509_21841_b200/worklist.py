@@ -81,10 +81,22 @@ class WorkList:
     segs: np.ndarray       # SEG_DTYPE
     pairs_per_head: int    # visible causal pairs for one query head
     kv_tiles: int          # sum over items of KV tiles walked
+    tile_pairs: np.ndarray | None = None  # visible pairs of each item's query tile (one head)
+    n_head_pairs: int = 1
 
     @property
     def n_items(self) -> int:
         return int(self.items.shape[0])
+
+    def cut(self, pairs_per_head: int) -> int:
+        """Item index (a whole-tile boundary) such that items [0, index)
+        cover about ``pairs_per_head`` visible pairs per head: the prefix a
+        rank runs to fill a predicted wait (longest tiles first)."""
+        if pairs_per_head <= 0 or self.tile_pairs is None or not self.n_items:
+            return 0
+        per_tile = self.tile_pairs[::self.n_head_pairs]
+        k = int(np.searchsorted(np.cumsum(per_tile), pairs_per_head, side="left")) + 1
+        return min(k, per_tile.shape[0]) * self.n_head_pairs
 
 
 def build_worklist(frags: list[QueryFragment], n_head_pairs: int,
@@ -122,6 +134,7 @@ def build_worklist(frags: list[QueryFragment], n_head_pairs: int,
         cols["state_row0"].append((f.state_row0 + offs[keep]) if f.state_row0 >= 0 else np.full(k, -1))
         cols["flags"].append(flags[keep])
         cols["cost"].append(cost[keep])
+        cols.setdefault("pairs", []).append(vis[keep])
     segs = np.zeros(max(len(seg_rows), 1), dtype=SEG_DTYPE)
     for i, row in enumerate(seg_rows):
         segs[i] = row
@@ -137,7 +150,7 @@ def build_worklist(frags: list[QueryFragment], n_head_pairs: int,
         items[name] = np.repeat(tiles[name][order], n_head_pairs)
     items["head_pair"] = np.tile(np.arange(n_head_pairs), n_tiles)
     kv_tiles = int(tiles["cost"].sum()) * n_head_pairs
-    return WorkList(items, segs, pairs, kv_tiles)
+    return WorkList(items, segs, pairs, kv_tiles, np.repeat(tiles["pairs"][order], n_head_pairs), n_head_pairs)
 
 
 # ------------------------------------------------------------------ backward

@@ -205,3 +205,59 @@ def test_bwd_program_covers_forward_pairs_with_disjoint_tiles(g):
                 tiles.add(key)
         for rp, up in zip(prog.rings, bp.unpack_ranges):
             assert np.array_equal(up[:, 0], rp.pack_ranges[:, 1]) and np.array_equal(up[:, 1], rp.pack_ranges[:, 0])
+
+
+def _makespan(schedule, num_ranks, fill):
+    """Cost-model makespan (pairs as time) of the ring list schedule with
+    ``fill[r][j]`` local pairs run by rank r before its j-th ring and the rest
+    after its last ring (reference simulator.py:136-187 ordering rules)."""
+    in_ring = {s.sequence_id for rs in schedule.rings() for s in rs.ring.sequences}
+    local = [0] * num_ranks
+    for t in schedule.local_tasks:
+        if t.sequence_id not in in_ring:
+            local[t.rank] += t.compute_pairs
+    t_now = [0] * num_ranks
+    left = list(local)
+    seen = [0] * num_ranks
+    for rs in schedule.rings():
+        members = rs.ring.members
+        for m in members:
+            take = fill[m][seen[m]]
+            t_now[m] += take
+            left[m] -= take
+            seen[m] += 1
+        start = max(t_now[m] for m in members)
+        end = start + max(sum(rd.compute_pairs for rd in rs.rounds[i]) for i in range(len(members)))
+        for m in members:
+            t_now[m] = end
+    return max(t + l for t, l in zip(t_now, left))
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_local_fill_never_lengthens_the_modelled_step(seed):
+    """program.local_fill_plan (locals fill predicted ring waits) against
+    "all locals first" under the same cost model: never longer, and every
+    rank's local items are split into in-order chunks that cover the list."""
+    from paper_2509_21841_b200.program import local_fill_plan
+    rng = np.random.default_rng(seed)
+    g = int(rng.choice([2, 3, 4, 5, 8]))
+    lengths = [int(x) for x in rng.integers(1, 6000, size=int(rng.integers(3, 14)))]
+    lengths.append(int(sum(lengths)))  # long enough to need a ring
+    total = sum(lengths)
+    plan = P.build_plan(SequenceBatch(tuple(enumerate(lengths))), ClusterSpec(1, g, -(-total * 105 // (100 * g)),
+                                                                              1.0, 1.0))
+    sched = S.build_schedule(plan)
+    fill = local_fill_plan(sched, g)
+    in_ring = {s.sequence_id for rs in sched.rings() for s in rs.ring.sequences}
+    local = [0] * g
+    for t in sched.local_tasks:
+        if t.sequence_id not in in_ring:
+            local[t.rank] += t.compute_pairs
+    first = {r: [local[r] if j == 0 else 0 for j in range(len(fill[r]))] for r in range(g)}
+    assert _makespan(sched, g, fill) <= _makespan(sched, g, first)
+    for r in range(g):
+        prog = build_rank_program(plan, sched, r, 4)
+        assert len(prog.local_cuts) == len(prog.rings)
+        assert all(a <= b for a, b in zip(prog.local_cuts, prog.local_cuts[1:]))
+        assert all(0 <= c <= prog.local.n_items and c % prog.n_head_pairs == 0 for c in prog.local_cuts)
+        assert sum(fill[r]) <= local[r]
