@@ -262,6 +262,12 @@ ZP_API int zp_ring_hop(void* dst, const void* src, int64_t bytes, const int32_t*
                 int32_t* consumed_flag, int32_t consumed_epoch, int32_t* next_full_flag,
                 int32_t next_full_epoch, void* stream);
 
+/* Stream-ordered device copy (copy engine; src may be a peer's IPC-mapped
+ * address: the ring backward pulls the predecessor's dK/dV partial sums with
+ * it between zp_stream_wait_flag / zp_stream_write_flag) and memset. */
+ZP_API int zp_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
+ZP_API int zp_memset_async(void* dst, int value, int64_t bytes, void* stream);
+
 /* ---- full transformer block (config 5): elementwise kernels around the
  * cuBLAS GEMMs of the linear modules, which run on the balanced (linear)
  * layout as in the reference's linear phase (simulator.py:291-299). */

@@ -49,7 +49,9 @@ SIGNATURES: dict[str, tuple] = {
     "zp_stream_write_flag": (_c_int, [_vp, ctypes.c_int32, _vp]),
     "zp_ring_hop": (_c_int, [_vp, _vp, _c_i64, _vp, ctypes.c_int32, _vp, ctypes.c_int32, _vp, ctypes.c_int32,
                              _vp, ctypes.c_int32, _vp]),
-    "zp_rmsnorm":(_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_float, _vp]),
+    "zp_memcpy_async": (_c_int, [_vp, _vp, _c_i64, _vp]),
+    "zp_memset_async": (_c_int, [_vp, _c_int, _c_i64, _vp]),
+    "zp_rmsnorm": (_c_int, [_vp, _vp, _vp, _c_int, _c_int, _c_float, _vp]),
     "zp_rope_split": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
     "zp_swiglu": (_c_int, [_vp, _vp, _c_int, _c_int, _vp]),
     "zp_ipc_get_handle": (_c_int, [_vp, _vp, ctypes.POINTER(_c_i64)]),

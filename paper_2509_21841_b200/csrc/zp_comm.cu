@@ -94,3 +94,22 @@ extern "C" int zp_ring_hop(void* dst, const void* src, int64_t bytes, const int3
   if (next_full_flag && (rc = write_flag(next_full_flag, next_full_epoch, s)) != ZP_OK) return rc;
   return ZP_OK;
 }
+
+extern "C" int zp_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes > 0 && (!dst || !src))) return zp_fail(ZP_EINVAL, "zp_memcpy_async: bad arguments");
+  if (bytes == 0) return ZP_OK;
+  if (zp_check_device() != ZP_OK) return ZP_ENODEV;
+  cudaError_t e = cudaMemcpyAsync(dst, src, size_t(bytes), cudaMemcpyDeviceToDevice,
+                                  reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_memcpy_async");
+  return ZP_OK;
+}
+
+extern "C" int zp_memset_async(void* dst, int value, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes > 0 && !dst)) return zp_fail(ZP_EINVAL, "zp_memset_async: bad arguments");
+  if (bytes == 0) return ZP_OK;
+  if (zp_check_device() != ZP_OK) return ZP_ENODEV;
+  cudaError_t e = cudaMemsetAsync(dst, value, size_t(bytes), reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return zp_fail_cuda(e, "zp_memset_async");
+  return ZP_OK;
+}

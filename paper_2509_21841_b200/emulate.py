@@ -89,81 +89,62 @@ def emulate_ranks_on_one_gpu(plan, sched, sq: dict, sk: dict, sv: dict, device="
 
 
 def emulate_backward_on_one_gpu(plan, sched, sq: dict, sk: dict, sv: dict, sdo: dict, outs, device="cuda"):
-    """Backward of ``emulate_ranks_on_one_gpu``: every rank's LocalTask and
-    ring-round gradients with ``zp_attn_bwd``; a ring's partial dK/dV travel
-    with its KV set (device copies instead of NCCL) and return to the owner
-    after the last round.  ``outs`` are the forward's (o, lse) per rank.
-    Returns [(dq, dk, dv) fp32] per rank in attention layout."""
+    """Every rank's attention_backward on one GPU through the production
+    executor (``engine.attention_backward_steps``): LocalTask gradients, ring
+    rounds with the KV sets pulled hop by hop and the dK/dV running totals
+    pulled, added and forwarded by the same copy-engine / flag protocol, the
+    own set's total returned after the last round.  ``outs`` are the
+    forward's (o, lse) per rank.  Returns [(dq, dk, dv) fp32] per rank in
+    attention layout."""
+    from .engine import BwdDeviceProgram, attention_backward_steps
     from .program import build_bwd_program
-    from .engine import BwdDeviceProgram
     hq = next(iter(sq.values())).shape[1]
     hkv, d = next(iter(sk.values())).shape[1:]
     scale = 1.0 / math.sqrt(d)
     dev = torch.device(device)
-    progs = [build_rank_program(plan, sched, r, hq) for r in range(plan.num_ranks)]
+    world = plan.num_ranks
+    ctxs = [RankContext(r, world, dev) for r in range(world)]
+    streams = [torch.cuda.Stream(dev) for _ in range(world)]
+    rows = ring_rows_needed(sched)
+    if rows:
+        ts = RingTransport.local_group(ctxs, rows, 2 * hkv * d * 2)
+        RingTransport.attach_grad_local(ts, rows, hkv * d)
+        for c, t in zip(ctxs, ts):
+            c.ring = t
+    progs = [build_rank_program(plan, sched, r, hq) for r in range(world)]
     devs = [DeviceProgram(p, dev) for p in progs]
     bdevs = [BwdDeviceProgram(build_bwd_program(p, hkv), dev) for p in progs]
-    q = [gather_rank(sq, plan, r, device) for r in range(plan.num_ranks)]
-    k = [gather_rank(sk, plan, r, device) for r in range(plan.num_ranks)]
-    v = [gather_rank(sv, plan, r, device) for r in range(plan.num_ranks)]
-    do = [gather_rank(sdo, plan, r, device) for r in range(plan.num_ranks)]
+    q = [gather_rank(sq, plan, r, dev) for r in range(world)]
+    k = [gather_rank(sk, plan, r, dev) for r in range(world)]
+    v = [gather_rank(sv, plan, r, dev) for r in range(world)]
+    do = [gather_rank(sdo, plan, r, dev) for r in range(world)]
     grads, deltas = [], []
-    for r, bd in enumerate(bdevs):
+    for r in range(world):
         o, lse = outs[r]
         delta = torch.empty_like(lse)
         if progs[r].rows:
             ops.attn_bwd_prep(o, do[r], delta)
-        dq = torch.zeros(q[r].shape, dtype=torch.float32, device=dev)
-        dk = torch.zeros(k[r].shape, dtype=torch.float32, device=dev)
-        dv = torch.zeros(k[r].shape, dtype=torch.float32, device=dev)
-        if bd.local.n:
-            ops.attn_bwd(q[r], k[r], v[r], do[r], lse, delta, dq, dk, dv, bd.local.items, bd.local.n,
-                         bd.local.segs, softmax_scale=scale)
-        grads.append((dq, dk, dv))
         deltas.append(delta)
+        grads.append(tuple(torch.zeros(x.shape, dtype=torch.float32, device=dev) for x in (q[r], k[r], k[r])))
+    torch.cuda.synchronize(dev)
+    gens = [attention_backward_steps(plan, sched, q[r], k[r], v[r], do[r], outs[r][1], deltas[r], *grads[r],
+                                     ctxs[r], progs[r], bdevs[r], devs[r], scale) for r in range(world)]
+
+    def advance(r):
+        with torch.cuda.stream(streams[r]):
+            return next(gens[r], None)
+
     for ri, rs in enumerate(sched.rings()):
-        members = rs.ring.members
-        g = len(members)
-        idx = {m: next(j for j, x in enumerate(progs[m].rings) if x.ring_index == ri) for m in members}
-        held, gk, gv = {}, {}, {}
-        for m in members:
-            rp = progs[m].rings[idx[m]]
-            pack = devs[m].rings[idx[m]][0]
-            rows = max(rp.held_rows)
-            buf = torch.zeros(rows, 2, hkv, d, dtype=torch.bfloat16, device=dev)
-            n = rp.pack_ranges.shape[0]
-            mx = int(rp.pack_ranges[:, 2].max()) if n else 0
-            ops.copy_rows(buf[:, 0], k[m], pack, n, mx)
-            ops.copy_rows(buf[:, 1], v[m], pack, n, mx)
-            held[m] = buf
-            gk[m] = torch.zeros(rows, hkv, d, dtype=torch.float32, device=dev)
-            gv[m] = torch.zeros(rows, hkv, d, dtype=torch.float32, device=dev)
-        for rnd in range(g):
-            for m in members:
-                rp = progs[m].rings[idx[m]]
-                work = bdevs[m].rings[idx[m]][0][rnd]
-                n_kv = rp.rounds[rnd].kv_rows
-                if work.n:
-                    ops.attn_bwd(q[m], held[m][:n_kv, 0], held[m][:n_kv, 1], do[m], outs[m][1], deltas[m],
-                                 grads[m][0], gk[m][:n_kv], gv[m][:n_kv], work.items, work.n, work.segs,
-                                 softmax_scale=scale)
-            nh, nk, nv = {}, {}, {}
-            for m in members:
-                rp = progs[m].rings[idx[m]]
-                n = rp.send_rows(rnd)
-                nh[rp.next_rank] = held[m][:n].clone()
-                nk[rp.next_rank] = gk[m][:n].clone()
-                nv[rp.next_rank] = gv[m][:n].clone()
-            held, gk, gv = nh, nk, nv
-        for m in members:
-            rp = progs[m].rings[idx[m]]
-            up = bdevs[m].rings[idx[m]][1]
-            n = up.numel() // 3
-            mx = int(rp.pack_ranges[:, 2].max()) if n else 0
-            if n:
-                ops.copy_rows(grads[m][1], gk[m], up, n, mx)
-                ops.copy_rows(grads[m][2], gv[m], up, n, mx)
-    torch.cuda.synchronize()
+        for step in range(rs.ring.group_size + 2):
+            for m in rs.ring.members:
+                tag = advance(m)
+                if tag != (ri, step):
+                    raise AssertionError(f"rank {m}: expected ring step {(ri, step)}, got {tag}")
+            torch.cuda.synchronize(dev)  # every flag the next step waits for is written
+    for r in range(world):
+        while advance(r) is not None:
+            pass
+    torch.cuda.synchronize(dev)
     return grads
 
 

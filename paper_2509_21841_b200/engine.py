@@ -201,33 +201,20 @@ class DeviceProgram:
         self.h2d_bytes = host.nbytes
 
 
-def ring_p2p_ops(rp, round_index: int, cur: torch.Tensor, nxt: torch.Tensor, group=None) -> list:
-    """Point-to-point ops after ring round ``round_index``: forward the held KV
-    set to position i+1 and receive the next one from i-1 (reference
-    attention_engine.py:247-251).  Zero-row transfers are skipped on both
-    sides (the counts are plan-determined)."""
-    ops_ = []
-    n_send, n_recv = rp.send_rows(round_index), rp.recv_rows(round_index)
-    if n_send:
-        ops_.append(dist.P2POp(dist.isend, cur[:n_send], rp.next_rank, group))
-    if n_recv:
-        ops_.append(dist.P2POp(dist.irecv, nxt[:n_recv], rp.prev_rank, group))
-    return ops_
-
-
-
-
 class RingTransport:
     """One rank's ring KV buffers and epoch flags, plus the peers' addresses.
 
     ``n_buf`` buffers of ``rows`` KV rows (K and V interleaved per row, 4 KiB
     per token at Llama-3 shapes) in one allocation, and an int32 flag block
-    ``[0, world)`` "full from predecessor p", ``[world, 2*world)`` "consumed by
-    successor s".  Peers reach both over NVLink through CUDA IPC
-    (``create``, collective), or — ranks emulated in one process on one GPU —
-    through plain device pointers (``local_group``).  The hop itself is
-    ``zp_ring_hop``: stream-ordered flag waits / writes and one copy-engine
-    pull, no SM (RingHop describes the protocol)."""
+    ``[0, world)`` "KV set full from predecessor p", ``[world, 2*world)`` "KV
+    set consumed by successor s", ``[2*world, 3*world)`` "dK/dV partial sum
+    ready from predecessor p", ``[3*world, 4*world)`` "partial sum consumed by
+    successor s" (the last two for the backward's gradient buffers, attached
+    on the first backward call).  Peers reach everything over NVLink through
+    CUDA IPC (``create`` / ``attach_grad``, collective), or — ranks emulated in
+    one process on one GPU — through plain device pointers (``local_group``).
+    A hop is ``zp_ring_hop``: stream-ordered flag waits / writes and one
+    copy-engine pull, no SM (RingHop describes the protocol)."""
 
     N_BUF = 3
 
@@ -235,9 +222,13 @@ class RingTransport:
         self.ctx = ctx
         self.rows, self.row_bytes = rows, row_bytes
         self.storage = torch.empty(self.N_BUF * max(rows, 1) * row_bytes, dtype=torch.uint8, device=ctx.device)
-        self.flags = torch.zeros(2 * ctx.world, dtype=torch.int32, device=ctx.device)
+        self.flags = torch.zeros(4 * ctx.world, dtype=torch.int32, device=ctx.device)
         self.buf_base: list[int] = []   # per rank: address of its storage (this process's mapping)
         self.flag_base: list[int] = []  # per rank: address of its flag block
+        self.gstorage: torch.Tensor | None = None  # N_GRAD fp32 dK/dV partial-sum buffers
+        self.grad_base: list[int] = []
+        self.grad_rows = 0
+        self.grad_elems = 0  # hkv * d
 
     def fits(self, rows: int, row_bytes: int) -> bool:
         return rows <= self.rows and row_bytes == self.row_bytes
@@ -273,6 +264,50 @@ class RingTransport:
         n = self.rows * self.row_bytes
         return self.storage[j * n:(j + 1) * n].view(torch.bfloat16).view(self.rows, 2, hkv, d)
 
+    N_GRAD = 3
+
+    def _grad_alloc(self, rows: int, elems: int) -> None:
+        self.grad_rows, self.grad_elems = rows, elems
+        self.gstorage = torch.empty(self.N_GRAD * 2 * max(rows, 1) * elems, dtype=torch.float32,
+                                    device=self.ctx.device)
+
+    def grad_fits(self, rows: int, elems: int) -> bool:
+        return self.gstorage is not None and rows <= self.grad_rows and elems == self.grad_elems
+
+    def attach_grad(self, rows: int, elems: int) -> None:
+        """Collective: allocate this rank's dK/dV partial-sum buffers and
+        exchange their IPC handles."""
+        self._grad_alloc(rows, elems)
+        ctx = self.ctx
+        torch.cuda.synchronize(ctx.device)
+        everyone = [None] * ctx.world
+        dist.all_gather_object(everyone, _ipc_export(self.gstorage), group=ctx.group)
+        self.grad_base = [self.gstorage.data_ptr() if r == ctx.rank else _ipc_open(h, o)
+                          for r, (h, o) in enumerate(everyone)]
+        dist.barrier(group=ctx.group)
+
+    @staticmethod
+    def attach_grad_local(ts: list["RingTransport"], rows: int, elems: int) -> None:
+        for t in ts:
+            t._grad_alloc(rows, elems)
+        for t in ts:
+            t.grad_base = [x.gstorage.data_ptr() for x in ts]
+
+    def grad_buffer(self, j: int, hkv: int, d: int) -> torch.Tensor:
+        """[2 (dK, dV), grad_rows, hkv, d] fp32 view of partial-sum buffer j."""
+        n = 2 * self.grad_rows * self.grad_elems
+        return self.gstorage[j * n:(j + 1) * n].view(2, self.grad_rows, hkv, d)
+
+    def grad_addr(self, rank: int, j: int, half: int) -> int:
+        """Address of rank's partial-sum buffer j, dK (half 0) or dV (half 1)."""
+        return self.grad_base[rank] + 4 * self.grad_elems * self.grad_rows * (2 * j + half)
+
+    def gfull_flag(self, owner: int, sender: int) -> int:
+        return self.flag_base[owner] + 4 * (2 * self.ctx.world + sender)
+
+    def gcons_flag(self, owner: int, reader: int) -> int:
+        return self.flag_base[owner] + 4 * (3 * self.ctx.world + reader)
+
     def buf_addr(self, rank: int, j: int) -> int:
         return self.buf_base[rank] + j * self.rows * self.row_bytes
 
@@ -301,6 +336,62 @@ def _ensure_ring_transport(ctx: RankContext, schedule, hkv: int, d: int) -> Ring
     return ctx.ring
 
 
+def _pack_and_announce(ctx: RankContext, rp, epoch0: int, dev_pack, k, v, bufs) -> None:
+    """Own KV set -> transport buffer 0, announced to the successor (epoch
+    offset 0); this ring's hops start after the pack (event edge): they
+    refill buffers the previous ring's rounds read, and their flag writes
+    must land after the pack's (a flag only grows)."""
+    from . import _native
+    T, xs = ctx.ring, ctx.comm_stream
+    n_pack = rp.pack_ranges.shape[0]
+    max_pack = int(rp.pack_ranges[:, 2].max()) if n_pack else 0
+    cs = torch.cuda.current_stream()
+    ops.copy_rows(bufs[0][:, 0], k, dev_pack, n_pack, max_pack)
+    ops.copy_rows(bufs[0][:, 1], v, dev_pack, n_pack, max_pack)
+    _native.call("zp_stream_write_flag", T.full_flag(rp.next_rank, ctx.rank), epoch0, int(cs.cuda_stream))
+    packed = torch.cuda.Event()
+    packed.record(cs)
+    xs.wait_event(packed)
+
+
+def _kv_hop(ctx: RankContext, rp, epoch0: int, h, done: dict) -> torch.cuda.Event:
+    """Hop h (program.RingHop) on the comm stream: the predecessor's set
+    -> own buffer h.dst_buf.  Returns the event the round that reads it waits
+    for."""
+    from . import _native
+    T, xs = ctx.ring, ctx.comm_stream
+    me, pred, succ = ctx.rank, rp.prev_rank, rp.next_rank
+    if h.free is not None:
+        xs.wait_event(done[h.free])  # the dst buffer's last local reader
+    if ctx.tracer is not None:
+        # traced step: wait for the flags first, so the span times the copy alone
+        _native.call("zp_stream_wait_flag", T.full_flag(me, pred), epoch0 + h.full, int(xs.cuda_stream))
+        if h.free is not None:
+            _native.call("zp_stream_wait_flag", T.consumed_flag(me, succ), epoch0 + h.free, int(xs.cuda_stream))
+    with ctx.span("intra-comm", "kv.send", {"ring": rp.ring_index, "round": h.round_index, "tokens": h.rows,
+                                             "bytes": h.rows * T.row_bytes, "src": pred}, xs):
+        _native.call("zp_ring_hop", T.buf_addr(me, h.dst_buf), T.buf_addr(pred, h.src_buf),
+                     h.rows * T.row_bytes, T.full_flag(me, pred), epoch0 + h.full,
+                     T.consumed_flag(me, succ) if h.free is not None else None,
+                     epoch0 + (h.free or 0), T.consumed_flag(pred, me), epoch0 + h.consumed,
+                     T.full_flag(succ, me) if h.next_full is not None else None,
+                     epoch0 + (h.next_full or 0), int(xs.cuda_stream))
+    ev = torch.cuda.Event()
+    ev.record(xs)
+    return ev
+
+
+def _leave_ring(ctx: RankContext, rp, epoch0: int) -> None:
+    """Leave the ring only after the successor pulled its last set from us
+    (the next ring refills buffer 0); later work on the compute stream waits."""
+    from . import _native
+    xs = ctx.comm_stream
+    if rp.group_size >= 2:
+        _native.call("zp_stream_wait_flag", ctx.ring.consumed_flag(ctx.rank, rp.next_rank),
+                     epoch0 + rp.group_size - 2, int(xs.cuda_stream))
+    torch.cuda.current_stream().wait_stream(xs)
+
+
 def _ring_steps(ctx: RankContext, rp, epoch0: int, dev_pack, dev_rounds, q, k, v, o, lse, scale):
     """One ring at this position, as a generator: yields after the pack and
     after each round is enqueued (the single-GPU emulation interleaves the
@@ -312,29 +403,15 @@ def _ring_steps(ctx: RankContext, rp, epoch0: int, dev_pack, dev_rounds, q, k, v
     held from position (i - r) mod g (reference attention_engine.py:229-244),
     resuming the running softmax state; hop r pulls the next set from the
     predecessor (attention_engine.py:247-251) while round r runs."""
-    from . import _native
     T = ctx.ring
     hkv, d = k.shape[1], k.shape[2]
     hq = q.shape[1]
-    g, me, pred, succ = rp.group_size, ctx.rank, rp.prev_rank, rp.next_rank
-    xs = ctx.comm_stream
+    g = rp.group_size
     parity = v.dtype == torch.float16
     bufs = [T.buffer(j, hkv, d) for j in range(rp.n_buffers)]
     st_o = ctx.workspace("ring_state_o", (max(rp.state_rows, 1), hq, d), torch.float32)
     st_ml = ctx.workspace("ring_state_ml", (2, hq, max(rp.state_rows, 1)), torch.float32)
-    n_pack = rp.pack_ranges.shape[0]
-    max_pack = int(rp.pack_ranges[:, 2].max()) if n_pack else 0
-    cs = torch.cuda.current_stream()
-    # own set -> buffer 0, announced to the successor (epoch offset 0)
-    ops.copy_rows(bufs[0][:, 0], k, dev_pack, n_pack, max_pack)
-    ops.copy_rows(bufs[0][:, 1], v, dev_pack, n_pack, max_pack)
-    _native.call("zp_stream_write_flag", T.full_flag(succ, me), epoch0, int(cs.cuda_stream))
-    # this ring's hops start after the pack: they refill buffers the previous
-    # ring's rounds read, and their flag writes must land after the pack's
-    # (a flag only grows)
-    packed = torch.cuda.Event()
-    packed.record(cs)
-    xs.wait_event(packed)
+    _pack_and_announce(ctx, rp, epoch0, dev_pack, k, v, bufs)
     yield
     hops = rp.hops()
     ready: dict[int, torch.cuda.Event] = {}
@@ -342,26 +419,7 @@ def _ring_steps(ctx: RankContext, rp, epoch0: int, dev_pack, dev_rounds, q, k, v
     for r in range(g):
         cs = torch.cuda.current_stream()
         if r < g - 1:
-            h = hops[r]
-            if h.free is not None:
-                xs.wait_event(done[h.free])  # the dst buffer's last local reader
-            if ctx.tracer is not None:
-                # traced step: wait for the flags first, so the span times the copy alone
-                _native.call("zp_stream_wait_flag", T.full_flag(me, pred), epoch0 + h.full, int(xs.cuda_stream))
-                if h.free is not None:
-                    _native.call("zp_stream_wait_flag", T.consumed_flag(me, succ), epoch0 + h.free,
-                                 int(xs.cuda_stream))
-            with ctx.span("intra-comm", "kv.send", {"ring": rp.ring_index, "round": r, "tokens": h.rows,
-                                                     "bytes": h.rows * T.row_bytes, "src": pred}, xs):
-                _native.call("zp_ring_hop", T.buf_addr(me, h.dst_buf), T.buf_addr(pred, h.src_buf),
-                             h.rows * T.row_bytes, T.full_flag(me, pred), epoch0 + h.full,
-                             T.consumed_flag(me, succ) if h.free is not None else None,
-                             epoch0 + (h.free or 0), T.consumed_flag(pred, me), epoch0 + h.consumed,
-                             T.full_flag(succ, me) if h.next_full is not None else None,
-                             epoch0 + (h.next_full or 0), int(xs.cuda_stream))
-            ev = torch.cuda.Event()
-            ev.record(xs)
-            ready[r + 1] = ev
+            ready[r + 1] = _kv_hop(ctx, rp, epoch0, hops[r], done)
         if r > 0:
             cs.wait_event(ready[r])
         work = dev_rounds[r]
@@ -377,11 +435,7 @@ def _ring_steps(ctx: RankContext, rp, epoch0: int, dev_pack, dev_rounds, q, k, v
         ev.record(cs)
         done[r] = ev
         yield
-    # leave the ring only after the successor pulled its last set from us
-    # (the next ring refills buffer 0); rounds after this wait on the stream
-    if g >= 2:
-        _native.call("zp_stream_wait_flag", T.consumed_flag(me, succ), epoch0 + g - 2, int(xs.cuda_stream))
-    torch.cuda.current_stream().wait_stream(xs)
+    _leave_ring(ctx, rp, epoch0)
 
 
 def _run_ring_allgather(ctx: RankContext, rp, dev_pack, dev_rounds, q, k, v, o, lse, scale):
@@ -522,95 +576,117 @@ class BwdDeviceProgram:
         self.rings = [([_DevWork(view(a), view(b), n) for a, b, n in rounds], view(up)) for rounds, up in rings]
 
 
-def _run_ring_backward(ctx: RankContext, rp, dev_pack, dev_rounds, dev_unpack, q, k, v, dout, lse, delta,
-                       dq, dk, dv, scale):
-    """Ring backward.  Round r computes dQ (accumulated in place) and this
-    position's contribution Z_r to dK/dV of the KV set it holds, into fresh
-    buffers.  On the comm stream, while round r+1 computes, the partial sum A_r
-    received from position i-1 is added (T_r = A_r + Z_r) and forwarded to
-    i+1, and the KV set for round r+2 moves one hop; after the last round the
-    same exchange returns every set's total gradient to its owner (the
-    reference charges g sends per ring, README.md:119-124).  The compute
-    stream waits only for KV sets, never for gradients."""
+def _ring_bwd_steps(ctx: RankContext, rp, epoch0: int, dev_pack, dev_rounds, dev_unpack, q, k, v, dout, lse,
+                    delta, dq, dk, dv, scale):
+    """Ring backward at this position, as a generator (steps as in
+    ``_ring_steps``).  The KV sets travel exactly as in the forward.  Round r
+    computes dQ (accumulated in place) and this position's share Z_r of the
+    dK/dV of the set it holds, into partial-sum buffer r % 3.  On the comm
+    stream, once round r is done, the running total A_r of that set is pulled
+    from the predecessor (its buffer of round r-1, a copy-engine read over
+    NVLink), added (T_r = Z_r + A_r, ``zp_add_f32``) and announced to the
+    successor, which pulls it for round r+1; after the last round the
+    predecessor's total of this position's own set is pulled and unpacked into
+    dk / dv — the reference charges g sends per ring (README.md:119-124), the
+    backward uses all of them.  The compute stream never waits for gradients,
+    except before refilling a partial-sum buffer the successor has not pulled
+    yet (three buffers)."""
+    from . import _native
+    T = ctx.ring
     hkv, d = k.shape[1], k.shape[2]
-    g = rp.group_size
-    rows = max(rp.held_rows)
-    cs, xs = torch.cuda.current_stream(), ctx.comm_stream
-    kv = [ctx.workspace(f"ringkv{j}", (rows, 2, hkv, d), torch.bfloat16) for j in (0, 1)]
-    # own contribution (z) and received partial (a) for dK and dV, fp32, double-buffered
-    zk = [ctx.workspace(f"ring_zk{j}", (rows, hkv, d), torch.float32) for j in (0, 1)]
-    zv = [ctx.workspace(f"ring_zv{j}", (rows, hkv, d), torch.float32) for j in (0, 1)]
-    ak = [ctx.workspace(f"ring_ak{j}", (rows, hkv, d), torch.float32) for j in (0, 1)]
-    av = [ctx.workspace(f"ring_av{j}", (rows, hkv, d), torch.float32) for j in (0, 1)]
-    n_pack = rp.pack_ranges.shape[0]
-    max_pack = int(rp.pack_ranges[:, 2].max()) if n_pack else 0
-    ops.copy_rows(kv[0][:, 0], k, dev_pack, n_pack, max_pack)
-    ops.copy_rows(kv[0][:, 1], v, dev_pack, n_pack, max_pack)
-    start = torch.cuda.Event()
-    start.record(cs)
-    xs.wait_event(start)  # buffers (fresh from the compute stream's pool) and the packed set are ready
-    kv_ready = start
-    z_free = [None, None]
+    g, me, pred, succ = rp.group_size, ctx.rank, rp.prev_rank, rp.next_rank
+    xs = ctx.comm_stream
+    xsp = int(xs.cuda_stream)
+    bufs = [T.buffer(j, hkv, d) for j in range(rp.n_buffers)]
+    gz = [T.grad_buffer(j, hkv, d) for j in range(T.N_GRAD)]
+    ga = [ctx.workspace(f"ring_ga{j}", (2, T.grad_rows, hkv, d), torch.float32) for j in (0, 1)]
+    half = T.grad_elems * 4  # bytes per row of one half (dK or dV)
+    _pack_and_announce(ctx, rp, epoch0, dev_pack, k, v, bufs)
+    yield
+    hops = rp.hops()
+    ready: dict[int, torch.cuda.Event] = {}
+    done: dict[int, torch.cuda.Event] = {}
+
+    def pull_total(r_src: int, rows: int, into: torch.Tensor) -> None:
+        # the predecessor's running total of its round r_src (buffer r_src % 3)
+        _native.call("zp_stream_wait_flag", T.gfull_flag(me, pred), epoch0 + r_src, xsp)
+        for hf in (0, 1):
+            _native.call("zp_memcpy_async", into[hf].data_ptr(), T.grad_addr(pred, r_src % T.N_GRAD, hf),
+                         rows * half, xsp)
+        _native.call("zp_stream_write_flag", T.gcons_flag(pred, me), epoch0 + r_src, xsp)
+
     for r in range(g):
-        cur, nxt = r % 2, (r + 1) % 2
-        # -- KV set for round r+1 moves one hop (overlaps this round's compute)
-        next_kv = None
+        cs = torch.cuda.current_stream()
         if r < g - 1:
-            with torch.cuda.stream(xs), ctx.span("intra-comm", "kv.send",
-                                                  {"ring": rp.ring_index, "round": r, "tokens": rp.send_rows(r),
-                                                   "dst": rp.next_rank}, xs):
-                p2p = ring_p2p_ops(rp, r, kv[cur], kv[nxt], ctx.group)
-                if p2p:
-                    for req in dist.batch_isend_irecv(p2p):
-                        req.wait()
-            next_kv = torch.cuda.Event()
-            next_kv.record(xs)
-        # -- this round's gradients into fresh buffers
-        n_kv = rp.rounds[r].kv_rows
+            ready[r + 1] = _kv_hop(ctx, rp, epoch0, hops[r], done)
         if r > 0:
-            cs.wait_event(kv_ready)
-        if z_free[cur] is not None:
-            cs.wait_event(z_free[cur])  # what these buffers held two rounds ago has been forwarded
-        zk[cur][:n_kv].zero_()
-        zv[cur][:n_kv].zero_()
+            cs.wait_event(ready[r])
+        n_kv = rp.rounds[r].kv_rows
+        z = gz[r % T.N_GRAD]
+        if r >= T.N_GRAD:  # the successor pulled what this buffer held (T_{r-3})
+            _native.call("zp_stream_wait_flag", T.gcons_flag(me, succ), epoch0 + r - T.N_GRAD,
+                         int(cs.cuda_stream))
+        for hf in (0, 1):
+            _native.call("zp_memset_async", z[hf].data_ptr(), 0, n_kv * half, int(cs.cuda_stream))
         work = dev_rounds[r]
+        buf = bufs[r % rp.n_buffers]
         with ctx.span("compute", "intra_node.attn_bwd",
                       {"ring": rp.ring_index, "round": r, "pairs": rp.rounds[r].work.pairs_per_head}):
             if work.n:
-                ops.attn_bwd(q, kv[cur][:n_kv, 0], kv[cur][:n_kv, 1], dout, lse, delta, dq, zk[cur][:n_kv],
-                             zv[cur][:n_kv], work.items, work.n, work.segs, softmax_scale=scale)
-        done = torch.cuda.Event()
-        done.record(cs)
-        # -- add the partial received for this set and forward it (comm stream)
-        n_send, n_recv = rp.send_rows(r), rp.recv_rows(r)
-        with torch.cuda.stream(xs), ctx.span("intra-comm", "dkv.send",
-                                              {"ring": rp.ring_index, "round": r, "tokens": n_send,
-                                               "dst": rp.next_rank}, xs):
-            xs.wait_event(done)
-            if r > 0 and n_send:
-                ops.add_f32_(zk[cur][:n_send], ak[cur][:n_send])
-                ops.add_f32_(zv[cur][:n_send], av[cur][:n_send])
-            p2p = []
-            if n_send:
-                p2p += [dist.P2POp(dist.isend, zk[cur][:n_send], rp.next_rank, ctx.group),
-                        dist.P2POp(dist.isend, zv[cur][:n_send], rp.next_rank, ctx.group)]
-            if n_recv:
-                p2p += [dist.P2POp(dist.irecv, ak[nxt][:n_recv], rp.prev_rank, ctx.group),
-                        dist.P2POp(dist.irecv, av[nxt][:n_recv], rp.prev_rank, ctx.group)]
-            if p2p:
-                for req in dist.batch_isend_irecv(p2p):
-                    req.wait()
+                ops.attn_bwd(q, buf[:n_kv, 0], buf[:n_kv, 1], dout, lse, delta, dq, z[0][:n_kv], z[1][:n_kv],
+                             work.items, work.n, work.segs, softmax_scale=scale)
         ev = torch.cuda.Event()
-        ev.record(xs)
-        z_free[cur] = ev
-        if next_kv is not None:
-            kv_ready = next_kv
-    cs.wait_stream(xs)
-    own = g % 2  # the return hop delivered this rank's own set total into a*[own]
+        ev.record(cs)
+        done[r] = ev
+        # running total of the held set: + what the previous holders accumulated
+        xs.wait_event(ev)
+        with ctx.span("intra-comm", "dkv.send", {"ring": rp.ring_index, "round": r, "tokens": n_kv}, xs):
+            if r > 0:
+                a = ga[r % 2]
+                pull_total(r - 1, n_kv, a)
+                ops.add_f32_(z[0][:n_kv], a[0][:n_kv], stream=xs)
+                ops.add_f32_(z[1][:n_kv], a[1][:n_kv], stream=xs)
+            _native.call("zp_stream_write_flag", T.gfull_flag(succ, me), epoch0 + r, xsp)
+        yield
+    # this position's own set: its total arrives from the predecessor's last round
+    own = rp.held_rows[rp.position]
+    a = ga[g % 2]
+    pull_total(g - 1, own, a)
     n_up = dev_unpack.numel() // 3
     if n_up:
-        ops.copy_rows(dk, ak[own], dev_unpack, n_up, max_pack)
-        ops.copy_rows(dv, av[own], dev_unpack, n_up, max_pack)
+        max_up = int(rp.pack_ranges[:, 2].max())
+        ops.copy_rows(dk, a[0], dev_unpack, n_up, max_up, stream=xs)
+        ops.copy_rows(dv, a[1], dev_unpack, n_up, max_up, stream=xs)
+    yield  # (step g+1: every member has pulled its own total)
+    # the successor pulled our last total too, before the buffers are reused
+    _native.call("zp_stream_wait_flag", T.gcons_flag(me, succ), epoch0 + g - 1, xsp)
+    _leave_ring(ctx, rp, epoch0)
+
+
+def _ensure_ring_grad(ctx: RankContext, schedule, hkv: int, d: int) -> None:
+    rows = ring_rows_needed(schedule)
+    T = ctx.ring
+    if not T.grad_fits(rows, hkv * d):
+        T.attach_grad(max(rows, int(1.25 * T.grad_rows)) if T.gstorage is not None else rows, hkv * d)
+
+
+def attention_backward_steps(plan, schedule, q, k, v, dout, lse, delta, dq, dk, dv, ctx: RankContext,
+                             prog: RankProgram, bdev: "BwdDeviceProgram", devp: "DeviceProgram", scale: float):
+    """Generator form of ``attention_backward`` (fp32 dq / dk / dv given):
+    LocalTask gradients, then every ring in ``schedule.rings()`` order;
+    yields ``(ring_index, step)`` with steps 0 (pack) .. g (rounds) and g+1
+    (own total pulled)."""
+    epoch = ctx.ring_epoch
+    ctx.ring_epoch += 16 * len(schedule.rings())  # the same on every rank
+    if bdev.local.n:
+        with ctx.span("compute", "local.attn_bwd", {"pairs": bdev.bp.local.pairs_per_head}):
+            ops.attn_bwd(q, k, v, dout, lse, delta, dq, dk, dv, bdev.local.items, bdev.local.n, bdev.local.segs,
+                         softmax_scale=scale)
+    for i, rp in enumerate(prog.rings):
+        rounds, unpack = bdev.rings[i]
+        for step, _ in enumerate(_ring_bwd_steps(ctx, rp, epoch + 16 * rp.ring_index, devp.rings[i][0], rounds,
+                                                 unpack, q, k, v, dout, lse, delta, dq, dk, dv, scale)):
+            yield rp.ring_index, step
 
 
 def attention_backward(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
@@ -619,7 +695,8 @@ def attention_backward(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torc
                        softmax_scale: float | None = None):
     """Gradients of this rank's attention (the backward of ``attention_forward``
     with the same plan).  o / lse are the forward outputs (final LSE).
-    Returns (dq, dk, dv) bf16 in the rank's attention layout."""
+    Returns (dq, dk, dv) bf16 in the rank's attention layout.  Collective when
+    the plan has rings (every rank calls it with the same plan)."""
     ctx = ctx or RankContext.from_env()
     hq, hkv = q.shape[1], k.shape[1]
     prog = program or build_rank_program(plan, schedule, ctx.rank, hq)
@@ -632,14 +709,13 @@ def attention_backward(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torc
     dq = torch.zeros(q.shape, dtype=torch.float32, device=q.device)
     dk = torch.zeros(k.shape, dtype=torch.float32, device=q.device)
     dv = torch.zeros(k.shape, dtype=torch.float32, device=q.device)
-    if bdev.local.n:
-        with ctx.span("compute", "local.attn_bwd", {"pairs": bdev.bp.local.pairs_per_head}):
-            ops.attn_bwd(q, k, v, dout, lse, delta, dq, dk, dv, bdev.local.items, bdev.local.n, bdev.local.segs,
-                         softmax_scale=scale)
-    devp = DeviceProgram(prog, q.device) if prog.rings else None
-    for i, rp in enumerate(prog.rings):
-        rounds, unpack = bdev.rings[i]
-        _run_ring_backward(ctx, rp, devp.rings[i][0], rounds, unpack, q, k, v, dout, lse, delta, dq, dk, dv, scale)
+    devp = DeviceProgram(prog, q.device)
+    if ctx.world > 1 and schedule.rings():
+        _ensure_ring_transport(ctx, schedule, hkv, k.shape[2])
+        _ensure_ring_grad(ctx, schedule, hkv, k.shape[2])
+    for _ in attention_backward_steps(plan, schedule, q, k, v, dout, lse, delta, dq, dk, dv, ctx, prog, bdev,
+                                      devp, scale):
+        pass
     return dq.to(torch.bfloat16), dk.to(torch.bfloat16), dv.to(torch.bfloat16)
 
 
