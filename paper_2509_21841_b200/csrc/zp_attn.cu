@@ -176,7 +176,7 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 }
 
 #ifndef ZP_EMU_OF8
-#define ZP_EMU_OF8 1
+#define ZP_EMU_OF8 2
 #endif
 constexpr int kEmuOf8 = ZP_EMU_OF8;  // column pairs per 8 whose exp2 runs on the FMA pipe
 
