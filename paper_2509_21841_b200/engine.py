@@ -27,7 +27,6 @@ Public entry points (drop-in execution of what the reference only costs):
 from __future__ import annotations
 
 import math
-import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -38,7 +37,7 @@ import torch.distributed as dist
 from . import ops
 from .plan import build_plan
 from .program import BwdProgram, RankProgram, build_bwd_program, build_rank_program
-from .remap import RemapLayout, cost_matrix, remap_layout, solve_remap
+from .remap import RemapLayout, cost_matrix, solve_remap
 from .schedule import build_schedule
 from .worklist import BwdWorkList, WorkList
 
