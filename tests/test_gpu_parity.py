@@ -112,7 +112,7 @@ def test_parity_mode_is_the_same_pipeline():
     assert (lse_p - lse_b).abs().max().item() <= 1e-4
 
 
-@pytest.mark.parametrize("g", [2, 4])
+@pytest.mark.parametrize("g", [2, 4, 8])
 def test_c3_ring_within_north_star_tolerance(g):
     """Config 3 at full size (65,536 tokens per rank, one 131,072-token
     sequence split over a ring): every rank's LocalTasks and ring rounds run
