@@ -503,7 +503,8 @@ class CpuLayer:
         # the gather index of every linear-layout row (oracle rule R3)
         from oracle import remap as OR
         src = OR.source_map(list(self.lay.attn_rows), self.lay.matrix)
-        self.x = [torch.randn(n, 4096, generator=g) for n in self.lay.attn_rows] if world > 1 else []
+        self.x = ([torch.randn(n, 4096, generator=g).to(torch.bfloat16) for n in self.lay.attn_rows]
+                  if world > 1 else [])  # remap payload: hidden 4096 bf16 rows, as on the GPU
         self.gather = [(torch.from_numpy(np.ascontiguousarray(s[:, 0])), torch.from_numpy(np.ascontiguousarray(s[:, 1])))
                        for s in src] if world > 1 else []
         self.pairs = sum(n * (n + 1) // 2 for _, n in self.seqs)
@@ -540,7 +541,7 @@ class CpuLayer:
         if limit_tokens is None:
             for j in range(self.world if self.x else 0):
                 ranks, rows = self.gather[j]
-                out = torch.empty(len(rows), 4096)
+                out = torch.empty(len(rows), 4096, dtype=torch.bfloat16)
                 for r in range(self.world):
                     sel = (ranks == r).nonzero().squeeze(1)
                     if sel.numel():

@@ -124,10 +124,13 @@ class ZeppelinBlock:
         self.schedule = build_schedule(self.plan)
         self.program = build_rank_program(self.plan, self.schedule, r, self.hq, lay)
         if not hasattr(self, "_stagers"):
-            self._stagers = [engine.TableStager(self.ctx.device) for _ in range(2)]
+            self._stagers = [engine.TableStager(self.ctx.device) for _ in range(3)]
         self.device_program = engine.DeviceProgram(self.program, self.ctx.device, self._stagers[0])
         self.layout = self.program.remap
         self.pos = self._stagers[1].upload(np.ascontiguousarray(attention_positions(self.plan, r)))
+        # both remap tables of the step in one staged upload (no pinned allocation per call)
+        self._pull = (engine.pull_table_pair(self.layout, r, self._stagers[2])
+                      if self.peer_qkv is not None and self.layout.moved_rows() else (None, None))
         return self.plan
 
     @property
@@ -150,7 +153,7 @@ class ZeppelinBlock:
             else:
                 qkv = torch.matmul(h, w.w_qkv.t())
         if self.peer_qkv is not None:
-            engine.remap_pull(self.layout, self.peer_qkv, qkv_buf, ctx, inverse=True)
+            engine.remap_pull(self.layout, self.peer_qkv, qkv_buf, ctx, inverse=True, tables=self._pull[1])
             qkv = qkv_buf[:a]
         with ctx.span("compute", "rope", {"tokens": a}):
             q, k, v = ops.rope_split(qkv, self.pos, self.cos, self.sin, self.hq, self.hkv)
@@ -163,7 +166,8 @@ class ZeppelinBlock:
         engine.attention_forward(self.plan, self.schedule, q, k, v, ctx, self.program, self.device_program,
                                  out=(o, lse), kv_exchange="allgather" if self.strategy == "llama_cp" else "ring")
         if self.peer_o is not None:
-            engine.remap_pull(self.layout, self.peer_o, o_buf, ctx)
+            engine.remap_pull(self.layout, self.peer_o, o_buf, ctx, tables=self._pull[0])
+            self._stagers[2].release()  # both readers of this step's remap tables are enqueued
         with ctx.span("compute", "linear", {"tokens": b, "op": "o+mlp"}):
             x2 = torch.addmm(x, o_buf[:b], w.w_o.t())
             h2 = ops.rmsnorm(x2, w.mlp_norm, EPS)
