@@ -140,8 +140,7 @@ ZP_API int zp_attn_bwd_prep(const void* o, const void* dout, int rows, int hq, i
  * accumulate).  q, dout: [q_rows, hq, 128] bf16 (row-contiguous); k, v as in
  * zp_attn_fwd; lse (natural log, the forward's FINAL value) and delta:
  * [hq, lse_stride] fp32.  dq: [q_rows, hq, 128] fp32, ACCUMULATED with
- * atomic adds (zero it before the first call), or NULL to skip dQ (then
- * zp_attn_bwd_dq computes it); dk, dv: [kv_rows, hkv, 128]
+ * atomic adds (zero it before the first call); dk, dv: [kv_rows, hkv, 128]
  * fp32, each item writes (or, with ZP_BWD_ACCUMULATE, adds to) its own rows —
  * items of one call must cover disjoint (key row, kv head) tiles. */
 ZP_API int zp_attn_bwd(const void* q, const void* k, const void* v, const void* dout, int q_rows,
@@ -149,18 +148,6 @@ ZP_API int zp_attn_bwd(const void* q, const void* k, const void* v, const void* 
                 const float* delta, int lse_stride, float* dq, float* dk, float* dv,
                 const zp_bwd_item* items, int n_items, const zp_kv_seg* qsegs,
                 float softmax_scale, void* stream);
-
-/* Query-stationary dQ pass of the backward: one CTA per work item = a tile
- * of <=128 query rows of ONE query head (zp_attn_item.head_pair holds the
- * head index) walking the KV segments like zp_attn_fwd; recomputes S and dP,
- * forms dS = P * (dP - Delta) and accumulates dQ = scale * dS K in TMEM, then
- * adds it to dq [q_rows, hq, 128] fp32 (read-modify-write; one owner per
- * (tile, head) per call).  Pair with zp_attn_bwd(..., dq = NULL, ...), which
- * then computes dK / dV only. */
-ZP_API int zp_attn_bwd_dq(const void* q, const void* k, const void* v, const void* dout, int q_rows,
-                   int kv_rows, int kv_row_stride, int hq, int hkv, int head_dim, const float* lse,
-                   const float* delta, int lse_stride, float* dq, const zp_attn_item* items,
-                   int n_items, const zp_kv_seg* segs, float softmax_scale, void* stream);
 
 /* Row-range copy with 16-byte vector loads/stores.  For each range i:
  * dst rows [dst_row0[i], +n_rows[i]) <- src rows [src_row0[i], +n_rows[i]).

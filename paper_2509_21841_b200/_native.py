@@ -31,8 +31,6 @@ SIGNATURES: dict[str, tuple] = {
     "zp_attn_bwd": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp,
                              _c_int, _vp, _vp, _vp, _vp, _c_int, _vp, _c_float, _vp]),
     "zp_add_f32": (_c_int, [_vp, _vp, _c_i64, _vp]),
-    "zp_attn_bwd_dq": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp,
-                                _c_int, _vp, _vp, _c_int, _vp, _c_float, _vp]),
     "zp_copy_rows": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_i64, _vp, _c_int, _c_int, _vp]),
     "zp_remap_push": (_c_int, [_vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                ctypes.c_int32, _c_int, _vp]),

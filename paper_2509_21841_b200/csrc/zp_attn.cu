@@ -37,14 +37,13 @@
 #include <cstdlib>
 
 #include "zp_ptx.cuh"
-#include "zp_tiles.cuh"
 #include "../../include/zeppelin_b200.h"
 
 namespace zp {
 
 constexpr int kHeadDim = 128;
 constexpr int kBM = 128;  // query rows per CTA tile
-constexpr int kBN = kTileKeys;  // key rows per tile (zp_tiles.cuh)
+constexpr int kBN = 128;  // key rows per tile
 constexpr int kThreads = 384;
 constexpr uint32_t kTileBytes = kBM * kHeadDim * 2;   // 32 KB
 constexpr uint32_t kBoxBytes = 128 * 64 * 2;          // 16 KB (one 64-column x 128-row TMA box)
@@ -132,6 +131,33 @@ struct AttnArgs {
   int hq;
   int group;  // hq / hkv
   float scale_log2;
+};
+
+// Walks the KV tiles an item needs, in order: tiles of each segment up to the
+// item's last visible key (causal pruning; fully-masked tiles never issued).
+struct TileCursor {
+  const zp_kv_seg* segs;
+  int s, first, end, max_qpos, ti, nt;
+  zp_kv_seg g, g0;  // g0: segs[first], handed over through the schedule ring
+  __device__ __forceinline__ TileCursor(const zp_kv_seg* sg, int b, int c, int mq)
+      : segs(sg), s(b - 1), first(-1), end(b + c), max_qpos(mq), ti(0), nt(0) {}
+  __device__ __forceinline__ TileCursor(const zp_kv_seg* sg, int b, int c, int mq, const zp_kv_seg& seg0)
+      : segs(sg), s(b - 1), first(b), end(b + c), max_qpos(mq), ti(0), nt(0), g0(seg0) {}
+  __device__ __forceinline__ bool next() {
+    if (++ti < nt) return true;
+    while (++s < end) {
+      g = s == first ? g0 : segs[s];
+      if (g.len > 0 && g.pos0 <= max_qpos) {
+        nt = (min(g.len, max_qpos - g.pos0 + 1) + kBN - 1) / kBN;
+        ti = 0;
+        return true;
+      }
+    }
+    return false;
+  }
+  __device__ __forceinline__ int row() const { return g.row0 + ti * kBN; }
+  __device__ __forceinline__ int pos() const { return g.pos0 + ti * kBN; }
+  __device__ __forceinline__ int valid() const { return min(kBN, g.len - ti * kBN); }
 };
 
 #ifndef ZP_RESCALE_LOG2

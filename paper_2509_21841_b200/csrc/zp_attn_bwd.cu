@@ -177,9 +177,6 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int cc) {
   return uint32_t((r >> 3) * 1024 + (r & 7) * 128 + ((cc ^ (r & 7)) << 4));
 }
 
-// kDQ = false: dK / dV only (dQ comes from the query-stationary pass,
-// zp_attn_bwd_dq.cu): no dQ^T MMA, no dS^T shared-memory tile, no reduction.
-template <bool kDQ>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
@@ -286,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0 && m < 256) ZP_BSTAMP(3072 + m * 4 + 0);
         mbar_wait(bar(B_QDO_FULL + qs), (m / kQStages) & 1);
         if (lane == 0 && m < 256) ZP_BSTAMP(3072 + m * 4 + 1);
-        if (kDQ && m >= 2) mbar_wait(bar(B_DQ_EMPTY + buf), ((m >> 1) - 1) & 1);  // dQ^T(m-2) drained
+        if (m >= 2) mbar_wait(bar(B_DQ_EMPTY + buf), ((m >> 1) - 1) & 1);  // dQ^T(m-2) drained
         if (lane == 0 && m < 256) ZP_BSTAMP(3072 + m * 4 + 2);
         tc_fence_after();
 #pragma unroll 1
@@ -319,13 +316,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_ts_w(tDK, tDP0 + 64 * buf + kk * 8, q_mn + q_step * qs + ((kk * 2048) >> 4), idesc_kv, acc);
         }
         tc_commit_w(bar(B_QDO_EMPTY + qs));
-        if constexpr (kDQ) {
 #pragma unroll 1
-          for (int kk = 0; kk < kBK / 16; ++kk)
-            mma_ss_w(tS0 + 64 * buf, k_mn + ((kk * 2048) >> 4), dst_mn + p_step * buf + ((kk * 2048) >> 4), idesc_q,
-                     kk > 0 ? 1u : 0u);
-          tc_commit_w(bar(B_DQ_FULL + buf));
-        }
+        for (int kk = 0; kk < kBK / 16; ++kk)
+          mma_ss_w(tS0 + 64 * buf, k_mn + ((kk * 2048) >> 4), dst_mn + p_step * buf + ((kk * 2048) >> 4), idesc_q,
+                 kk > 0 ? 1u : 0u);
+        tc_commit_w(bar(B_DQ_FULL + buf));
         tc_commit_w(bar(B_PDS_EMPTY + buf));
         if (lane == 0 && n < 256) ZP_BSTAMP(2048 + n * 4 + 1);
       }
@@ -407,13 +402,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // they are the TMEM A operands of dV += P^T dO and dK += dS^T Q.
         tmem_st16(tS0 + lane_bits + 64 * buf + 16 * c, pk);
         tmem_st16(tDP0 + lane_bits + 64 * buf + 16 * c, dk);
-        if constexpr (kDQ) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            st_shared_v4(dst_row + sw128_off(k, 4 * c + i), dk[4 * i], dk[4 * i + 1], dk[4 * i + 2], dk[4 * i + 3]);
-        }
+        for (int i = 0; i < 4; ++i)
+          st_shared_v4(dst_row + sw128_off(k, 4 * c + i), dk[4 * i], dk[4 * i + 1], dk[4 * i + 2], dk[4 * i + 3]);
       }
-      if constexpr (kDQ) fence_proxy_async_smem();  // generic-proxy smem writes -> tcgen05.mma operands
+      fence_proxy_async_smem();  // generic-proxy smem writes -> tcgen05.mma operands
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
@@ -453,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (kDQ && warp >= 8) {
+  } else if (warp >= 8) {
     // ---------------- dQ reduction (thread == head dim): the dQ^T tile goes
     // through a shared-memory staging tile ([64 queries][128 dims] as four
     // 32-dim boxes) and leaves with four TMA reduce-adds (atomic in L2).
@@ -573,9 +566,8 @@ extern "C" int zp_attn_bwd(const void* q, const void* k, const void* v, const vo
     return zp_fail(ZP_EINVAL, "zp_attn_bwd: bad sizes");
   if (n_items == 0) return ZP_OK;
   if (q_rows == 0 || kv_rows == 0) return zp_fail(ZP_EINVAL, "zp_attn_bwd: empty q or kv with items");
-  if (!q || !k || !v || !dout || !lse || !delta || !dk || !dv || !items || !qsegs)
+  if (!q || !k || !v || !dout || !lse || !delta || !dq || !dk || !dv || !items || !qsegs)
     return zp_fail(ZP_EINVAL, "zp_attn_bwd: null pointer");
-  const bool with_dq = dq != nullptr;  // null: dK / dV only (zp_attn_bwd_dq supplies dQ)
   if (zp_check_device() != ZP_OK) return ZP_ENODEV;
 
   CUtensorMap tq, tdo, tk, tv, tdq;
@@ -592,19 +584,17 @@ extern "C" int zp_attn_bwd(const void* q, const void* k, const void* v, const vo
   if ((rc = zp_make_tmap_2d_bf16(&tv, v, uint64_t(hkv) * kD, uint64_t(kv_rows), uint64_t(kv_row_stride) * 2, 64,
                                  kBK)) != ZP_OK)
     return rc;
-  if (with_dq &&
-      (rc = zp_make_tmap_2d_f32(&tdq, dq, uint64_t(hq) * kD, uint64_t(q_rows), uint64_t(hq) * kD * 4, 32, kBQ)) !=
-          ZP_OK)
+  if ((rc = zp_make_tmap_2d_f32(&tdq, dq, uint64_t(hq) * kD, uint64_t(q_rows), uint64_t(hq) * kD * 4, 32, kBQ)) !=
+      ZP_OK)
     return rc;
-  if (!with_dq) tdq = tq;  // unused by the kernel variant
-  static bool attr_done[64][2] = {};  // per device and variant: the attribute is per device and function
+  static bool attr_done[64] = {};  // per device: the attribute is per device and function
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return zp_fail(ZP_ENODEV, "zp_attn_bwd: device");
-  if (!attr_done[dev][with_dq]) {
-    cudaError_t e = cudaFuncSetAttribute(with_dq ? attn_bwd_kernel<true> : attn_bwd_kernel<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes));
+  if (!attr_done[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kSmemBytes));
     if (e != cudaSuccess) return zp_fail_cuda(e, "zp_attn_bwd: smem attribute");
-    attr_done[dev][with_dq] = true;
+    attr_done[dev] = true;
   }
   BwdArgs a;
   a.items = items;
@@ -620,12 +610,8 @@ extern "C" int zp_attn_bwd(const void* q, const void* k, const void* v, const vo
   a.group = hq / hkv;
   a.scale = softmax_scale;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
-  if (with_dq)
-    attn_bwd_kernel<true><<<n_items, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(tq, tdo, tk, tv,
-                                                                                                    tdq, a);
-  else
-    attn_bwd_kernel<false><<<n_items, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(tq, tdo, tk, tv,
-                                                                                                     tdq, a);
+  attn_bwd_kernel<<<n_items, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(tq, tdo, tk, tv, tdq,
+                                                                                              a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return zp_fail_cuda(e, "zp_attn_bwd: launch");
   return ZP_OK;

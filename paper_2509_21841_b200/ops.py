@@ -16,9 +16,6 @@ from . import _native
 from .worklist import BwdWorkList, QueryFragment, WorkList, build_bwd_worklist, build_worklist
 
 HEAD_DIM = 128
-# backward in two passes: key-stationary dK/dV (zp_attn_bwd without dQ) +
-# query-stationary dQ (zp_attn_bwd_dq); 0 = the fused key-stationary kernel
-BWD_DQ_PASS = int(__import__("os").environ.get("ZP_BWD_DQ_PASS", "0"))
 
 # Instrumentation: number of native kernel launches issued, and an optional
 # hook that receives CUDA events bracketing each attention launch (bench.py
@@ -158,14 +155,14 @@ def attn_bwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, dout: torch.Tens
     q/dout [Tq, Hq, 128] bf16; k/v [Tk, Hkv, 128] bf16 (row stride may exceed
     Hkv*128); lse/delta fp32 [Hq, >=Tq]; dq fp32 [Tq, Hq, 128] (accumulated),
     dk/dv fp32 [Tk, Hkv, 128] contiguous."""
-    _require_cuda(q, k, v, dout, lse, delta, dk, dv)
+    _require_cuda(q, k, v, dout, lse, delta, dq, dk, dv)
     tq, hq, d = q.shape
     tk, hkv, _ = k.shape
     if dout.shape != q.shape or not dout.is_contiguous() or q.stride() != (hq * d, d, 1):
         raise ValueError("q and dout must be row-contiguous [T, H, 128] of equal shape")
     if k.stride()[1:] != (d, 1) or v.stride() != k.stride() or v.shape != k.shape:
         raise ValueError("k/v must have contiguous heads and equal strides")
-    for t_, shape in (((dq, q.shape),) if dq is not None else ()) + ((dk, k.shape), (dv, k.shape)):
+    for t_, shape in ((dq, q.shape), (dk, k.shape), (dv, k.shape)):
         if t_.dtype != torch.float32 or t_.shape != shape or not t_.is_contiguous():
             raise ValueError("dq/dk/dv must be contiguous fp32 with the q/k shapes")
     if lse.stride() != delta.stride() or lse.dtype != torch.float32 or delta.dtype != torch.float32:
@@ -176,35 +173,8 @@ def attn_bwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, dout: torch.Tens
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
     _native.call("zp_attn_bwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(), tq, tk, k.stride(0),
-                 hq, hkv, d, lse.data_ptr(), delta.data_ptr(), lse.stride(0),
-                 dq.data_ptr() if dq is not None else None, dk.data_ptr(),
+                 hq, hkv, d, lse.data_ptr(), delta.data_ptr(), lse.stride(0), dq.data_ptr(), dk.data_ptr(),
                  dv.data_ptr(), items.data_ptr(), n_items, qsegs.data_ptr(), scale, _stream_ptr(stream))
-    if _hook is not None:
-        ev1.record()
-        _hook("zp_attn_bwd", ev0, ev1)
-
-
-def attn_bwd_dq(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, dout: torch.Tensor, lse: torch.Tensor,
-                delta: torch.Tensor, dq: torch.Tensor, items: torch.Tensor, n_items: int, segs: torch.Tensor,
-                softmax_scale: float | None = None, stream: torch.cuda.Stream | None = None) -> None:
-    """Query-stationary dQ pass (zp_attn_bwd_dq) over a per-head work list
-    (worklist.build_worklist(frags, n_heads): head_pair = head); dq fp32 is
-    accumulated."""
-    _require_cuda(q, k, v, dout, lse, delta, dq)
-    tq, hq, d = q.shape
-    tk, hkv, _ = k.shape
-    if dq.dtype != torch.float32 or dq.shape != q.shape or not dq.is_contiguous():
-        raise ValueError("dq must be contiguous fp32 with the q shape")
-    if k.stride()[1:] != (d, 1) or v.stride() != k.stride() or v.shape != k.shape:
-        raise ValueError("k/v must have contiguous heads and equal strides")
-    scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
-    _count_launch()
-    if _hook is not None:
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
-    _native.call("zp_attn_bwd_dq", q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(), tq, tk, k.stride(0),
-                 hq, hkv, d, lse.data_ptr(), delta.data_ptr(), lse.stride(0), dq.data_ptr(), items.data_ptr(),
-                 n_items, segs.data_ptr(), scale, _stream_ptr(stream))
     if _hook is not None:
         ev1.record()
         _hook("zp_attn_bwd", ev0, ev1)
@@ -225,13 +195,7 @@ def varlen_attention_backward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
     dk = torch.zeros(k.shape, dtype=torch.float32, device=q.device)
     dv = torch.zeros(k.shape, dtype=torch.float32, device=q.device)
     items, qsegs = upload_bwd_worklist(wl, q.device)
-    if BWD_DQ_PASS:
-        attn_bwd(q, k, v, dout, lse, delta, None, dk, dv, items, wl.n_items, qsegs, softmax_scale)
-        qw = build_worklist(local_fragments(seqlens), hq)
-        qi, qs = upload_worklist(qw, q.device)
-        attn_bwd_dq(q, k, v, dout, lse, delta, dq, qi, qw.n_items, qs, softmax_scale)
-    else:
-        attn_bwd(q, k, v, dout, lse, delta, dq, dk, dv, items, wl.n_items, qsegs, softmax_scale)
+    attn_bwd(q, k, v, dout, lse, delta, dq, dk, dv, items, wl.n_items, qsegs, softmax_scale)
     return dq.to(torch.bfloat16), dk.to(torch.bfloat16), dv.to(torch.bfloat16)
 
 

@@ -6,4 +6,4 @@ cd "$(dirname "$0")/../paper_2509_21841_b200/csrc"
 mkdir -p ../../build/variants
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
   -Xcompiler -fvisibility=hidden --use_fast_math -I../../include -shared "$@" \
-  zp_attn.cu zp_attn_bwd.cu zp_attn_bwd_dq.cu zp_move.cu zp_comm.cu zp_host.cu zp_block.cu -lcudart -o ../../build/variants/$name.so
+  zp_attn.cu zp_attn_bwd.cu zp_move.cu zp_comm.cu zp_host.cu zp_block.cu -lcudart -o ../../build/variants/$name.so
