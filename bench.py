@@ -305,6 +305,10 @@ def run_gpu(args):
             "rank_pairs": int(per_rank[busiest][2]),
             "attn_ms_per_step": per_rank[busiest][1],
             "aggregate_tflops": sum(r[2] for r in per_rank) * FLOP_PER_PAIR / (ms / 1e3) / 1e12,
+            # the step against the slowest rank's attention (ring waits, remap,
+            # planner-table uploads are what separate them)
+            "attn_ms_max_over_ranks": max(r[1] for r in per_rank),
+            "step_over_slowest_attention": ms / max(max(r[1] for r in per_rank), 1e-9),
         },
         "remap_stress": remap_stress,
         "gpu_launches": launches,

@@ -99,6 +99,7 @@ class _DevWork:
     items: torch.Tensor
     segs: torch.Tensor
     n: int
+    in_place: "_DevWork | None" = None  # ring round 0: the same items reading k / v in place
 
 
 class TableStager:
@@ -183,7 +184,8 @@ class DeviceProgram:
         rings = []
         for rp in prog.rings:
             pack = add(rp.pack_ranges)
-            rounds = [add_work(rr.work) for rr in rp.rounds]
+            rounds = [(add_work(rr.work), add_work(rr.work_in_place) if rr.work_in_place is not None else None)
+                      for rr in rp.rounds]
             rings.append((pack, rounds))
         host = np.concatenate(chunks) if chunks else np.zeros(1, np.int32)
         if stager is not None:
@@ -195,8 +197,12 @@ class DeviceProgram:
             off, n = span
             return self.table[off:off + n]
 
-        self.local = _DevWork(view(local[0]), view(local[1]), local[2])
-        self.rings = [(view(pack), [_DevWork(view(a), view(b), n) for a, b, n in rounds]) for pack, rounds in rings]
+        def dev_work(w, ip=None):
+            a, b, n = w
+            return _DevWork(view(a), view(b), n, dev_work(ip) if ip is not None else None)
+
+        self.local = dev_work(local)
+        self.rings = [(view(pack), [dev_work(w, ip) for w, ip in rounds]) for pack, rounds in rings]
         self.h2d_bytes = host.nbytes
 
 
@@ -391,26 +397,44 @@ def _leave_ring(ctx: RankContext, rp, epoch0: int) -> None:
     torch.cuda.current_stream().wait_stream(xs)
 
 
-def _ring_steps(ctx: RankContext, rp, epoch0: int, dev_pack, dev_rounds, q, k, v, o, lse, scale):
+def _ring_steps(ctx: RankContext, rp, epoch0: int, dev_pack, dev_rounds, q, k, v, o, lse, scale,
+                pack_after: torch.cuda.Event | None = None):
     """One ring at this position, as a generator: yields after the pack and
     after each round is enqueued (the single-GPU emulation interleaves the
     members' generators step by step, so every flag wait is enqueued after
-    the write it waits for).  Compute on the current stream, hops on the
-    context's comm stream (copy engines; no SM is taken from the rounds).
+    the write it waits for).  Compute on the current stream, the pack and the
+    hops on the context's comm stream (copy engines; no SM is taken from the
+    rounds).
 
     Per round r: attention of this position's query rows against the KV set
     held from position (i - r) mod g (reference attention_engine.py:229-244),
     resuming the running softmax state; hop r pulls the next set from the
-    predecessor (attention_engine.py:247-251) while round r runs."""
+    predecessor (attention_engine.py:247-251) while round r runs.  Round 0
+    (the position's own set) reads k / v in place, so it starts while the set
+    is being packed for the successor."""
+    from . import _native
     T = ctx.ring
     hkv, d = k.shape[1], k.shape[2]
     hq = q.shape[1]
-    g = rp.group_size
+    g, me, succ = rp.group_size, ctx.rank, rp.next_rank
+    xs = ctx.comm_stream
     parity = v.dtype == torch.float16
     bufs = [T.buffer(j, hkv, d) for j in range(rp.n_buffers)]
     st_o = ctx.workspace("ring_state_o", (max(rp.state_rows, 1), hq, d), torch.float32)
     st_ml = ctx.workspace("ring_state_ml", (2, hq, max(rp.state_rows, 1)), torch.float32)
-    _pack_and_announce(ctx, rp, epoch0, dev_pack, k, v, bufs)
+    # own set -> buffer 0 on the comm stream, announced to the successor
+    # (epoch offset 0); the hops follow on the same stream, so their flag
+    # writes land after the pack's (a flag only grows)
+    cs = torch.cuda.current_stream()
+    if pack_after is None:
+        pack_after = torch.cuda.Event()
+        pack_after.record(cs)  # k / v final; the previous ring's rounds no longer read buffer 0
+    xs.wait_event(pack_after)
+    n_pack = rp.pack_ranges.shape[0]
+    max_pack = int(rp.pack_ranges[:, 2].max()) if n_pack else 0
+    ops.copy_rows(bufs[0][:, 0], k, dev_pack, n_pack, max_pack, stream=xs)
+    ops.copy_rows(bufs[0][:, 1], v, dev_pack, n_pack, max_pack, stream=xs)
+    _native.call("zp_stream_write_flag", T.full_flag(succ, me), epoch0, int(xs.cuda_stream))
     yield
     hops = rp.hops()
     ready: dict[int, torch.cuda.Event] = {}
@@ -422,11 +446,15 @@ def _ring_steps(ctx: RankContext, rp, epoch0: int, dev_pack, dev_rounds, q, k, v
         if r > 0:
             cs.wait_event(ready[r])
         work = dev_rounds[r]
-        buf = bufs[r % rp.n_buffers]
-        n_kv = rp.rounds[r].kv_rows
         with ctx.span("compute", "intra_node.attn",
                       {"ring": rp.ring_index, "round": r, "pairs": rp.rounds[r].work.pairs_per_head}):
-            if work.n:
+            if r == 0 and work.in_place is not None:
+                w = work.in_place
+                if w.n:
+                    ops.attn_fwd(q, k, v, w.items, w.n, w.segs, o, lse, st_o, st_ml, softmax_scale=scale)
+            elif work.n:
+                buf = bufs[r % rp.n_buffers]
+                n_kv = rp.rounds[r].kv_rows
                 vv = buf[:n_kv, 1].view(torch.float16) if parity else buf[:n_kv, 1]
                 ops.attn_fwd(q, buf[:n_kv, 0], vv, work.items, work.n, work.segs, o, lse, st_o, st_ml,
                              softmax_scale=scale)
@@ -478,6 +506,10 @@ def attention_steps(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torch.T
     epoch = ctx.ring_epoch
     ctx.ring_epoch += 16 * len(schedule.rings())  # the same on every rank
     done = 0
+    # the first ring's pack needs only the inputs: it does not wait for the
+    # local work queued before the ring
+    inputs_ready = torch.cuda.Event()
+    inputs_ready.record(torch.cuda.current_stream())
 
     def local_items(upto: int):
         # LocalTask items [done, upto) of the longest-first list (zp_attn_fwd)
@@ -496,7 +528,7 @@ def attention_steps(plan, schedule, q: torch.Tensor, k: torch.Tensor, v: torch.T
             _run_ring_allgather(ctx, rp, pack, rounds, q, k, v, o, lse, scale)
             continue
         for step, _ in enumerate(_ring_steps(ctx, rp, epoch + 16 * rp.ring_index, pack, rounds, q, k, v, o,
-                                             lse, scale)):
+                                             lse, scale, pack_after=inputs_ready if j == 0 else None)):
             yield rp.ring_index, step
     local_items(devp.local.n)  # what is left runs after the last ring (simulator.py:181-187)
 

@@ -38,6 +38,10 @@ class RingRoundProgram:
     kv_rows: int            # rows of the KV set held this round
     work: WorkList
     frags: list[QueryFragment] = field(default_factory=list)  # query fragments vs the held KV
+    # round 0 only (the position's own KV set): the same items with segments in
+    # attention-layout rows, so the round reads k / v in place while the set
+    # is packed for the successor
+    work_in_place: WorkList | None = None
 
 
 @dataclass
@@ -261,7 +265,18 @@ def build_rank_program(plan, schedule: AttentionSchedule, rank: int, n_heads: in
             if wl.pairs_per_head != expect:
                 raise AssertionError(f"rank {rank} ring {ring.members} round {r}: work list covers "
                                      f"{wl.pairs_per_head} pairs, schedule says {expect}")
+            in_place = None
+            if src == i:
+                own = [QueryFragment(row0=f.row0, pos0=f.pos0, length=f.length, state_row0=f.state_row0,
+                                     segs=[(frag_rows[(sid, c)], c, d - c)
+                                           for c, d in seq_by_id[sid].ranges_by_position[i]])
+                       for (sid, _, _, _, _), f in zip(qf, frags)]
+                in_place = build_worklist(own, n_hp, tile_flags=flags)
+                if in_place.pairs_per_head != expect:
+                    raise AssertionError(f"rank {rank} ring {ring.members}: in-place round 0 covers "
+                                         f"{in_place.pairs_per_head} pairs, schedule says {expect}")
             prog.rounds.append(RingRoundProgram(round_index=r, src_position=src, kv_rows=held[src], work=wl,
+                                                work_in_place=in_place,
                                                 frags=frags))
         rings.append(prog)
 
