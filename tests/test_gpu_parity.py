@@ -98,6 +98,27 @@ def test_c2_full_batch_within_north_star_tolerance(preset):
     assert prod.lse_max_abs <= LSE_ABS and par.lse_max_abs <= LSE_ABS
 
 
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_c2_github_other_seeds(seed):
+    """Config 2's other batches (github preset, seeds 1-4; SURVEY 8(d) lists
+    seeds 0-4): the same two-clause tolerance, reference per sequence."""
+    seqlens = [n for _, n in W.c2_batch("github", seed).sequences]
+    q, k, v = _qkv(sum(seqlens), seed=100 + seed)
+    o_b, lse_b = ops.varlen_attention(q, k, v, seqlens)
+    o_p, lse_p = ops.varlen_attention(q, k, v.to(torch.float16), seqlens)
+    prod, par = ErrorStats(), ErrorStats()
+    r0 = 0
+    for n in seqlens:
+        s = slice(r0, r0 + n)
+        ro, rl = causal_attention_fp32(q[s], k[s], v[s])
+        prod.add(o_b[s], ro, lse_b[:, s], rl)
+        par.add(o_p[s], ro, lse_p[:, s], rl)
+        r0 += n
+    _record(f"c2_github_seed{seed}", {"seqlens": seqlens, "bf16": prod.as_dict(), "parity": par.as_dict()})
+    assert prod.max_abs <= MAX_ABS and par.mean_rel <= MEAN_REL, (prod.as_dict(), par.as_dict())
+    assert prod.lse_max_abs <= LSE_ABS and par.lse_max_abs <= LSE_ABS
+
+
 def test_parity_mode_is_the_same_pipeline():
     """The parity output rounded to bf16 is within one bf16 ulp-scale of the
     production output (same items, schedule and softmax; only the P/V operand

@@ -63,16 +63,17 @@ def test_fused_remap_matches_oracle_permutation(name, lay, method):
         assert torch.equal(back[r], xs[r]), (name, method, r)
 
 
-@pytest.mark.parametrize("method", ["pull", "push"])
-def test_fused_remap_hidden_4096_round_trip(method):
-    """Config-4 row size (hidden 4096 bf16 = 8 KiB per token) on a plan
-    layout: forward equals the oracle's numpy move, inverse restores x."""
-    batch = W.c4_batch(total=65536)
-    cluster = W.cluster_for(batch, 4)
+@pytest.mark.parametrize("method,total,g", [("pull", 65536, 4), ("push", 65536, 4), ("pull", 262144, 8)])
+def test_fused_remap_hidden_4096_round_trip(method, total, g):
+    """Config-4 row size (hidden 4096 bf16 = 8 KiB per token) on plan
+    layouts, up to config 4's full 256K tokens over 8 ranks: forward equals
+    the oracle's numpy move, inverse restores x."""
+    batch = W.c4_batch(total=total)
+    cluster = W.cluster_for(batch, g)
     plan = P.build_plan(batch, cluster)
     lay = remap_layout(plan.tokens_per_rank, solve_remap(plan.tokens_per_rank, cost_matrix(cluster)))
-    g = torch.Generator(device="cuda").manual_seed(5)
-    xs = [torch.randn(n, 4096, device="cuda", generator=g, dtype=torch.bfloat16) for n in lay.attn_rows]
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    xs = [torch.randn(n, 4096, device="cuda", generator=gen, dtype=torch.bfloat16) for n in lay.attn_rows]
     ys = emulate_remap_on_one_gpu(lay, xs, method)
     want = OR.forward([x.view(torch.int16).cpu().numpy() for x in xs], lay.matrix)
     for r in range(lay.world):
