@@ -302,7 +302,7 @@ ZP_API int zp_attn_set_sm_reserve(int sms);
 /* Misc. */
 ZP_API const char* zp_last_error(void);
 ZP_API int zp_device_sm_count(void);
-ZP_API int zp_version(void);
+ZP_API int zp_version(void);  /* 2 since round 2 (parity kernel, ring hops, phased remap) */
 
 #ifdef __cplusplus
 }

@@ -102,7 +102,7 @@ int zp_make_tmap_2d_f32(CUtensorMap* map, const void* base, uint64_t cols, uint6
 
 extern "C" const char* zp_last_error(void) { return g_err; }
 
-extern "C" int zp_version(void) { return 1; }
+extern "C" int zp_version(void) { return 2; }  // 2: parity kernel, ring hops, phased remap, spin bound
 
 extern "C" int zp_device_sm_count(void) {
   int dev = 0, n = 0;

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     for n in declared():
         assert hasattr(lib, n), n
     assert set(declared()) == set(_native.SIGNATURES), "ctypes table out of sync with the header"
-    assert _native.lib().zp_version() == 1
+    assert _native.lib().zp_version() == 2
 
 
 def test_struct_layouts_match_header():
