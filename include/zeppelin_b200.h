@@ -17,9 +17,17 @@
  *                      remap kept-row/tail copies
  *                        attention_engine.py:247-251  (KV rotates i -> i+1)
  *                        remapping.py:187-245         (transfer matrix M rows)
- *   zp_remap_push      fused remap: rows of M[i][j] stored straight into peer
- *                      buffers over NVLink, then a signal flag per (sender,receiver)
+ *   zp_attn_fwd_parity the same compute with fp16 P / V and fp32 O: the checkable
+ *                      form of the north star's mean-rel 1e-3 tolerance
+ *   zp_ring_hop        one RingRound KV forward (position i -> i+1) as a pull by
+ *   (+ zp_stream_*)    i+1: stream-waited epoch flags + one copy-engine transfer
+ *                        attention_engine.py:237,247-251; simulator.py:150-174
+ *   zp_remap_pull/push fused remap: rows of M[i][j] moved between peer buffers
+ *                      over NVLink, bracketed by ready/done epoch flags
  *                        remapping.py:187-255, simulator.py:282-302,336-347
+ *   zp_attn_bwd        the backward the reference charges as a multiple of the
+ *   (+ zp_add_f32)     forward (topology.py:37, simulator.py:304); ring dK/dV
+ *                      totals travel with the KV sets (README.md:119-124)
  *
  * Conventions: all pointers are device pointers (except where noted); the
  * library never allocates device memory; every call is asynchronous on the
