@@ -21,6 +21,8 @@ from dataclasses import dataclass
 import numpy as np
 
 TILE = 128
+# item order: 1 = KV-head-major (default; DRAM 6.0 -> 1.3 GB and +2.5% on config 2), 0 = the head pairs of a tile adjacent (A/B knob)
+KV_MAJOR = int(__import__("os").environ.get("ZP_KV_MAJOR", "1"))
 ITEM_LOAD_STATE = 1
 ITEM_STORE_STATE = 2
 
@@ -89,14 +91,14 @@ class WorkList:
         return int(self.items.shape[0])
 
     def cut(self, pairs_per_head: int) -> int:
-        """Item index (a whole-tile boundary) such that items [0, index)
-        cover about ``pairs_per_head`` visible pairs per head: the prefix a
-        rank runs to fill a predicted wait (longest tiles first)."""
+        """Item index (even: item pairs stay together) such that items
+        [0, index) cover about ``pairs_per_head`` visible pairs per head: the
+        prefix a rank runs to fill a predicted wait."""
         if pairs_per_head <= 0 or self.tile_pairs is None or not self.n_items:
             return 0
-        per_tile = self.tile_pairs[::self.n_head_pairs]
-        k = int(np.searchsorted(np.cumsum(per_tile), pairs_per_head, side="left")) + 1
-        return min(k, per_tile.shape[0]) * self.n_head_pairs
+        covered = np.cumsum(self.tile_pairs) / self.n_head_pairs  # pairs per head, item by item
+        k = int(np.searchsorted(covered, pairs_per_head, side="left")) + 1
+        return min(k + (k & 1), self.n_items)
 
 
 def build_worklist(frags: list[QueryFragment], n_head_pairs: int,
@@ -142,15 +144,25 @@ def build_worklist(frags: list[QueryFragment], n_head_pairs: int,
         return WorkList(np.zeros(0, dtype=ITEM_DTYPE), segs, 0, 0)
     tiles = {k: np.concatenate(v) for k, v in cols.items()}
     n_tiles = tiles["q_row0"].shape[0]
-    # longest tiles first; the head pairs of one tile stay adjacent so CTAs
-    # running together share K/V tiles in L2.
-    order = np.argsort(-tiles["cost"], kind="stable")
+    order = np.argsort(-tiles["cost"], kind="stable")  # longest tiles first (LPT)
+    if KV_MAJOR and n_head_pairs % 2 == 0:
+        # KV-head-major: all tiles of head pairs (2g, 2g+1) — one KV head for
+        # GQA groups of 4 — longest first, then the next pair of head pairs;
+        # the units in flight together stream the same K/V, which then stays
+        # in L2 instead of being re-read from HBM
+        t_idx = np.tile(np.repeat(order, 2), n_head_pairs // 2)
+        hp = (np.repeat(np.arange(0, n_head_pairs, 2), 2 * n_tiles)
+              + np.tile(np.array([0, 1]), n_tiles * (n_head_pairs // 2)))
+    else:
+        # the head pairs of one tile adjacent
+        t_idx = np.repeat(order, n_head_pairs)
+        hp = np.tile(np.arange(n_head_pairs), n_tiles)
     items = np.zeros(n_tiles * n_head_pairs, dtype=ITEM_DTYPE)
     for name in ("q_row0", "q_pos0", "q_len", "seg_begin", "seg_count", "state_row0", "flags"):
-        items[name] = np.repeat(tiles[name][order], n_head_pairs)
-    items["head_pair"] = np.tile(np.arange(n_head_pairs), n_tiles)
+        items[name] = tiles[name][t_idx]
+    items["head_pair"] = hp
     kv_tiles = int(tiles["cost"].sum()) * n_head_pairs
-    return WorkList(items, segs, pairs, kv_tiles, np.repeat(tiles["pairs"][order], n_head_pairs), n_head_pairs)
+    return WorkList(items, segs, pairs, kv_tiles, tiles["pairs"][t_idx], n_head_pairs)
 
 
 # ------------------------------------------------------------------ backward

@@ -259,5 +259,5 @@ def test_local_fill_never_lengthens_the_modelled_step(seed):
         prog = build_rank_program(plan, sched, r, 4)
         assert len(prog.local_cuts) == len(prog.rings)
         assert all(a <= b for a, b in zip(prog.local_cuts, prog.local_cuts[1:]))
-        assert all(0 <= c <= prog.local.n_items and c % prog.n_head_pairs == 0 for c in prog.local_cuts)
+        assert all(0 <= c <= prog.local.n_items and c % 2 == 0 for c in prog.local_cuts)
         assert sum(fill[r]) <= local[r]
