@@ -23,6 +23,7 @@ import numpy as np
 TILE = 128
 # item order: 1 = KV-head-major (default; DRAM 6.0 -> 1.3 GB and +2.5% on config 2), 0 = the head pairs of a tile adjacent (A/B knob)
 KV_MAJOR = int(__import__("os").environ.get("ZP_KV_MAJOR", "1"))
+BWD_KV_MAJOR = int(__import__("os").environ.get("ZP_BWD_KV_MAJOR", "1"))  # backward list order (1 = KV-head-major; A/B knob)
 ITEM_LOAD_STATE = 1
 ITEM_STORE_STATE = 2
 
@@ -257,8 +258,16 @@ def build_bwd_worklist(frags: list[QueryFragment], n_kv_heads: int, flags: int =
     order = np.argsort(-tiles["cost"], kind="stable")
     n_tiles = order.shape[0]
     items = np.zeros(n_tiles * n_kv_heads, dtype=BWD_ITEM_DTYPE)
+    if BWD_KV_MAJOR:
+        # KV-head-major (longest tiles first within a head): the CTAs in flight
+        # read the same query heads' Q / dO and reduce into the same dQ rows
+        t_idx = np.tile(order, n_kv_heads)
+        heads = np.repeat(np.arange(n_kv_heads), n_tiles)
+    else:
+        t_idx = np.repeat(order, n_kv_heads)
+        heads = np.tile(np.arange(n_kv_heads), n_tiles)
     for name in ("kv_row0", "kv_pos0", "kv_len", "qseg_begin", "qseg_count"):
-        items[name] = np.repeat(tiles[name][order], n_kv_heads)
-    items["kv_head"] = np.tile(np.arange(n_kv_heads), n_tiles)
+        items[name] = tiles[name][t_idx]
+    items["kv_head"] = heads
     items["flags"] = flags
     return BwdWorkList(items, qsegs, pairs, int(tiles["cost"].sum()) * n_kv_heads)
