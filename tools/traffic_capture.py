@@ -34,16 +34,22 @@ def busiest_program(n):
 
 
 def algorithmic_bytes(prog):
-    """q, k, v read once, o + lse written once per launch (bf16 / fp32)."""
-    from paper_2509_21841_b200.worklist import WorkList  # noqa: F401
-    rows = prog.rows
-    local = rows * (32 + 16) * 128 * 2 + rows * 32 * 128 * 2 + rows * 32 * 4
-    ring = 0
+    """Bytes each launch must move once: local — q, k, v read, o (bf16) and
+    lse written; ring round r — its query rows and the held KV set read, the
+    fp32 running state (O, m, l) read unless r is the first round and written
+    unless it is the last, o + lse written by the last round."""
+    local_rows = sum(f.length for f in prog.local_frags)
+    total = local_rows * (32 + 16) * 128 * 2 + local_rows * 32 * (128 * 2 + 4)
     for rp in prog.rings:
-        for rr in rp.rounds:
+        g = rp.group_size
+        for r, rr in enumerate(rp.rounds):
             qrows = sum(f.length for f in rr.frags)
-            ring += qrows * 32 * 128 * 2 + rr.kv_rows * 16 * 128 * 2 + qrows * 32 * 128 * 4 * 2
-    return local + ring
+            state = qrows * 32 * (128 + 2) * 4
+            total += qrows * 32 * 128 * 2 + rr.kv_rows * 16 * 128 * 2
+            total += (state if r > 0 else 0) + (state if r < g - 1 else 0)
+            if r == g - 1:
+                total += qrows * 32 * (128 * 2 + 4)
+    return total
 
 
 def run(n):
