@@ -270,6 +270,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         StepCursor cur(args.qsegs, it.qseg_begin, it.qseg_count, it.kv_pos0, args.group);
         while (cur.next()) ++n_steps;
       }
+      // The step count comes from global loads, so ptxas cannot prove it
+      // warp-uniform; REDUX returns it in a uniform register, which makes the
+      // step loop uniform and lets every descriptor below live in uniform
+      // registers (UIADD3.64 per MMA instead of an R2UR chain: the issue loop
+      // was the backward's critical path, ~88 cycles per MMA).
+      n_steps = int(__reduce_max_sync(0xffffffffu, unsigned(n_steps)));
       mbar_wait(bar(B_KV), 0);
       tc_fence_after();
 #ifdef ZP_TRACE
@@ -286,13 +292,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (m >= 2) mbar_wait(bar(B_DQ_EMPTY + buf), ((m >> 1) - 1) & 1);  // dQ^T(m-2) drained
         if (lane == 0 && m < 256) ZP_BSTAMP(3072 + m * 4 + 2);
         tc_fence_after();
-#pragma unroll 1
+#pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk) {
           const uint64_t ao = ((kk >> 2) * kKVBox + (kk & 3) * 32) >> 4;
           const uint64_t bo = ((kk >> 2) * kQBox + (kk & 3) * 32) >> 4;
           mma_ss_w(tS0 + 64 * buf, k_kmaj + ao, q_kmaj + q_step * qs + bo, idesc_t, kk > 0 ? 1u : 0u);
         }
-#pragma unroll 1
+#pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk) {
           const uint64_t ao = ((kk >> 2) * kKVBox + (kk & 3) * 32) >> 4;
           const uint64_t bo = ((kk >> 2) * kQBox + (kk & 3) * 32) >> 4;
@@ -308,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(bar(B_PDS_FULL + buf), (n >> 1) & 1);
         tc_fence_after();
         if (lane == 0 && n < 256) ZP_BSTAMP(2048 + n * 4 + 0);
-#pragma unroll 1
+#pragma unroll
         for (int kk = 0; kk < kBQ / 16; ++kk) {
           const uint32_t acc = (n > 0 || kk > 0) ? 1u : 0u;
           // A = P^T / dS^T straight from TMEM (bf16x2, 8 columns per 16 queries)
@@ -316,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_ts_w(tDK, tDP0 + 64 * buf + kk * 8, q_mn + q_step * qs + ((kk * 2048) >> 4), idesc_kv, acc);
         }
         tc_commit_w(bar(B_QDO_EMPTY + qs));
-#pragma unroll 1
+#pragma unroll
         for (int kk = 0; kk < kBK / 16; ++kk)
           mma_ss_w(tS0 + 64 * buf, k_mn + ((kk * 2048) >> 4), dst_mn + p_step * buf + ((kk * 2048) >> 4), idesc_q,
                  kk > 0 ? 1u : 0u);
