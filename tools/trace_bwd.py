@@ -30,6 +30,8 @@ mm = a[2048:3072].reshape(256, 4)[lo:hi]
 print(f"softmax: wait SDP {np.median(sm[:,1]-sm[:,0]):.0f}  wait PDS_EMPTY {np.median(sm[:,2]-sm[:,1]):.0f}  compute+arrive {np.median(sm[:,3]-sm[:,2]):.0f}  period {np.median(np.diff(sm[:,3])):.0f}")
 print(f"mma: PDS seen -> dQ issued {np.median(mm[:,1]-mm[:,0]):.0f}; softmax arrive -> MMA sees PDS {np.median(mm[:,0]-sm[:,3]):.0f}; period {np.median(np.diff(mm[:,0])):.0f}")
 print(f"dq warps: drain+reds {np.median(dqw[:,1]-dqw[:,0]):.0f}; MMA dQ issued -> DQ_FULL seen {np.median(dqw[:,0]-mm[:,1]):.0f}")
+print(f"dq warps (warp 8): DQ_FULL -> own box free {np.median(dqw[:,2]-dqw[:,0]):.0f}; -> stores done + reduce issued "
+      f"{np.median(dqw[:,1]-dqw[:,2]):.0f}; period {np.median(np.diff(dqw[:,0])):.0f}")
 sd = a[3072:4096].reshape(256, 4)[lo:hi]
 print(f"issue_sdp(m): wait QDO_FULL {np.median(sd[:,1]-sd[:,0]):.0f}  wait DQ_EMPTY {np.median(sd[:,2]-sd[:,1]):.0f}  issue 16 MMAs {np.median(sd[:,3]-sd[:,2]):.0f}")
 print(f"S^T(m) issued -> softmax sees SDP(m) {np.median(sm[:,1]-sd[:,3]):.0f}")
