@@ -473,6 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Query rows past the segment end carry exact zeros (P = dS = 0 there).
     const int quad = warp & 3;
     const uint32_t lane_bits = uint32_t(quad * 32) << 16;
+    const uint32_t box = sbase + kSmemDQ + quad * kDQBox;
     // Each warp owns one 32-dim box and issues its own reduce: a box waits
     // only for its own previous reduce, with no 128-thread barrier (one issuer
     // for all four boxes measured 6% slower on 64K).
