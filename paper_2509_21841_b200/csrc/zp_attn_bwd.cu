@@ -10,9 +10,9 @@
 //
 //   P  = exp(S*scale - LSE),  S = Q K^T
 //   dV += P^T dO
-//   dS  = P * (dO V^T - Delta)
-//   dK += scale * dS^T Q
-//   dQ += scale * dS K
+//   dS  = scale * P * (dO V^T - Delta)   (the scale folded into dS once)
+//   dK += dS^T Q
+//   dQ += dS K
 //
 // CTA = one work item = 128 keys of one KV head (KV-tile stationary) against
 // every query block (64 rows) of every query head of the GQA group that can see
@@ -94,6 +94,11 @@ struct BwdArgs {
   int group;
   float scale;
   float scale_log2;
+};
+
+template <bool B>
+struct BoolC {
+  static constexpr bool value = B;
 };
 
 // Steps of an item: query segments in order, 64-row blocks from the first one
@@ -349,6 +354,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool kval = k < it.kv_len;
     const int kpos = it.kv_pos0 + k;
     const float c1 = args.scale_log2;
+    // dS^T carries the softmax scale (dS' = scale * P * (dP - Delta)), so dK
+    // and dQ leave their accumulators unscaled
+    const float sc = args.scale;
     const uint32_t ld_base = sbase + kSmemLD + quad * 512;
     int n = 0;
     StepCursor cur(args.qsegs, it.qseg_begin, it.qseg_count, it.kv_pos0, args.group);
@@ -378,8 +386,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       st_shared_f32(ld_base + lane * 4, nl[0] * 1.4426950408889634f);
       st_shared_f32(ld_base + (32 + lane) * 4, nl[1] * 1.4426950408889634f);
-      st_shared_f32(ld_base + 256 + lane * 4, nd[0]);
-      st_shared_f32(ld_base + 256 + (32 + lane) * 4, nd[1]);
+      st_shared_f32(ld_base + 256 + lane * 4, nd[0] * sc);
+      st_shared_f32(ld_base + 256 + (32 + lane) * 4, nd[1] * sc);
       __syncwarp();
       if (ahead.next()) fetch(ahead);
       const int tr = (lane == 0 && quad == 0 && n < 256) ? n * 4 : -1;
@@ -391,41 +399,55 @@ __global__ void __launch_bounds__(kThreads, 1)
       ZP_BSTAMP(tr < 0 ? -1 : tr + 2);
       const bool full = kval && it.kv_len == kBK && qpos0 >= it.kv_pos0 + kBK - 1;
       const uint32_t dst_row = sbase + kSmemDST + buf * kPTile;
+      // Full steps (every query of the step sees every key of the item: the
+      // common case away from the diagonal) run a mask-free copy of the loop.
+      auto p_ds = [&](auto kFull) {
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t sr[32], dr[32];
-        tmem_ld32(tS0 + lane_bits + 64 * buf + 32 * c, sr);
-        tmem_ld32(tDP0 + lane_bits + 64 * buf + 32 * c, dr);
-        tmem_wait_ld();
-        uint32_t pk[16], dk[16];
+        for (int c = 0; c < 2; ++c) {
+          uint32_t sr[32], dr[32];
+          tmem_ld32(tS0 + lane_bits + 64 * buf + 32 * c, sr);
+          tmem_ld32(tDP0 + lane_bits + 64 * buf + 32 * c, dr);
+          tmem_wait_ld();
+          uint32_t pk[16], dk[16];
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          float lv[4], dv[4];
-          ld_shared_v4f(ld_base + (32 * c + j) * 4, lv);
-          ld_shared_v4f(ld_base + 256 + (32 * c + j) * 4, dv);
-          float p[4], ds[4];
+          for (int j = 0; j < 32; j += 4) {
+            float lv[4], dv[4];
+            ld_shared_v4f(ld_base + (32 * c + j) * 4, lv);
+            ld_shared_v4f(ld_base + 256 + (32 * c + j) * 4, dv);
+            float p[4], ds[4];
+            if constexpr (decltype(kFull)::value) {  // every (query, key) visible: no mask
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int q = 32 * c + j + u;
-            float e = ex2(__uint_as_float(sr[j + u]) * c1 - lv[u]);
-            if (!full && !(kval && qpos0 + q >= kpos)) e = 0.f;
-            p[u] = e;
-            ds[u] = e * (__uint_as_float(dr[j + u]) - dv[u]);
+              for (int u = 0; u < 4; ++u) {
+                p[u] = ex2(__uint_as_float(sr[j + u]) * c1 - lv[u]);
+                ds[u] = p[u] * (__uint_as_float(dr[j + u]) * sc - dv[u]);
+              }
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int q = 32 * c + j + u;
+                float e = ex2(__uint_as_float(sr[j + u]) * c1 - lv[u]);
+                if (!(kval && qpos0 + q >= kpos)) e = 0.f;
+                p[u] = e;
+                ds[u] = e * (__uint_as_float(dr[j + u]) * sc - dv[u]);
+              }
+            }
+            pk[j / 2] = pack_bf16(p[0], p[1]);
+            pk[j / 2 + 1] = pack_bf16(p[2], p[3]);
+            dk[j / 2] = pack_bf16(ds[0], ds[1]);
+            dk[j / 2 + 1] = pack_bf16(ds[2], ds[3]);
           }
-          pk[j / 2] = pack_bf16(p[0], p[1]);
-          pk[j / 2 + 1] = pack_bf16(p[2], p[3]);
-          dk[j / 2] = pack_bf16(ds[0], ds[1]);
-          dk[j / 2 + 1] = pack_bf16(ds[2], ds[3]);
-        }
-        // P^T / dS^T (bf16x2) over the S^T / dP^T columns this chunk has already
-        // read (chunk c covers columns [32c, 32c+32) and writes [16c, 16c+16));
-        // they are the TMEM A operands of dV += P^T dO and dK += dS^T Q.
-        tmem_st16(tS0 + lane_bits + 64 * buf + 16 * c, pk);
-        tmem_st16(tDP0 + lane_bits + 64 * buf + 16 * c, dk);
+          // P^T / dS^T (bf16x2) over the S^T / dP^T columns this chunk has already
+          // read (chunk c covers columns [32c, 32c+32) and writes [16c, 16c+16));
+          // they are the TMEM A operands of dV += P^T dO and dK += dS^T Q.
+          tmem_st16(tS0 + lane_bits + 64 * buf + 16 * c, pk);
+          tmem_st16(tDP0 + lane_bits + 64 * buf + 16 * c, dk);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          st_shared_v4(dst_row + sw128_off(k, 4 * c + i), dk[4 * i], dk[4 * i + 1], dk[4 * i + 2], dk[4 * i + 3]);
-      }
+          for (int i = 0; i < 4; ++i)
+            st_shared_v4(dst_row + sw128_off(k, 4 * c + i), dk[4 * i], dk[4 * i + 1], dk[4 * i + 2], dk[4 * i + 3]);
+        }
+      };
+      if (full) p_ds(BoolC<true>{});
+      else p_ds(BoolC<false>{});
       fence_proxy_async_smem();  // generic-proxy smem writes -> tcgen05.mma operands
       tmem_wait_st();
       tc_fence_before();
@@ -442,7 +464,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int which = 0; which < 2; ++which) {
         float4* dst = reinterpret_cast<float4*>((which ? args.dk : args.dv) + row * kD);
-        const float mul = which ? args.scale : 1.f;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t rr[32];
@@ -451,8 +472,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!kval) continue;
 #pragma unroll
           for (int v = 0; v < 8; ++v) {
-            float4 x = n > 0 ? make_float4(__uint_as_float(rr[4 * v]) * mul, __uint_as_float(rr[4 * v + 1]) * mul,
-                                           __uint_as_float(rr[4 * v + 2]) * mul, __uint_as_float(rr[4 * v + 3]) * mul)
+            float4 x = n > 0 ? make_float4(__uint_as_float(rr[4 * v]), __uint_as_float(rr[4 * v + 1]),
+                                           __uint_as_float(rr[4 * v + 2]), __uint_as_float(rr[4 * v + 3]))
                              : make_float4(0.f, 0.f, 0.f, 0.f);
             if (accum) {
               const float4 y = dst[8 * c + v];
@@ -495,9 +516,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0 && quad == 0 && n < 256) ZP_BSTAMP(1024 + n * 4 + 2);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) st_shared_f32(box + lane * 4 + j * 128, __uint_as_float(r0[j]) * args.scale);
+      for (int j = 0; j < 32; ++j) st_shared_f32(box + lane * 4 + j * 128, __uint_as_float(r0[j]));
 #pragma unroll
-      for (int j = 0; j < 32; ++j) st_shared_f32(box + lane * 4 + (32 + j) * 128, __uint_as_float(r1[j]) * args.scale);
+      for (int j = 0; j < 32; ++j) st_shared_f32(box + lane * 4 + (32 + j) * 128, __uint_as_float(r1[j]));
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
