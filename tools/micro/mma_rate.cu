@@ -6,7 +6,7 @@
 #include "../../paper_2509_21841_b200/csrc/zp_ptx.cuh"
 using namespace zp;
 
-template <int N, bool TS>
+template <int N, bool TS, int AMN = 0, int BMN = 0>
 __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t slot;
@@ -25,14 +25,19 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long
   const uint32_t tmem = slot;
   if (warp == 0) {
     const uint32_t base = (smem_u32(smem) + 1023u) & ~1023u;
-    const uint64_t a = umma_desc_sw128(base, 16, 1024);
-    const uint64_t b = umma_desc_sw128(base + 32768, 16, 1024);
-    constexpr uint32_t idesc = idesc_bf16_f32(128, N, 0, 0);
+    // K-major: LBO unused (16), SBO 1 KB between 8-row groups; MN-major: LBO =
+    // 16 KB between 64-element swizzle atoms along M/N, SBO 1 KB between 8-row
+    // groups along K (the backward's K^T / dS^T / dO operands)
+    const uint64_t a = umma_desc_sw128(base, AMN ? 16384 : 16, 1024);
+    const uint64_t b = umma_desc_sw128(base + 32768, BMN ? 16384 : 16, 1024);
+    constexpr uint32_t idesc = idesc_bf16_f32(128, N, AMN, BMN);
     const unsigned long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
-      const uint64_t off = uint64_t((i & 3) * 2);  // walk 32 B along K inside the atom
-      if constexpr (TS) mma_ts_w(tmem + 256, tmem, b + off, idesc, 1u);
-      else mma_ss_w(tmem, a + off, b + off, idesc, 1u);
+      // walk along K: 32 B inside the atom (K-major) or 2 KB = 16 rows (MN-major)
+      const uint64_t offa = AMN ? uint64_t((i & 3) * 128) : uint64_t((i & 3) * 2);
+      const uint64_t offb = BMN ? uint64_t((i & 3) * 128) : uint64_t((i & 3) * 2);
+      if constexpr (TS) mma_ts_w(tmem + 256, tmem, b + offb, idesc, 1u);
+      else mma_ss_w(tmem, a + offa, b + offb, idesc, 1u);
     }
     tc_commit_w(smem_u32(&bar));
     mbar_wait(smem_u32(&bar), 0);
@@ -45,9 +50,9 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
-template <int N, bool TS>
+template <int N, bool TS, int AMN = 0, int BMN = 0>
 void run(int sms, unsigned long long* d, int iters) {
-  auto k = mma_rate<N, TS>;
+  auto k = mma_rate<N, TS, AMN, BMN>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   k<<<sms, 128, 100 * 1024>>>(iters, d);
   cudaError_t e = cudaDeviceSynchronize();
@@ -56,7 +61,8 @@ void run(int sms, unsigned long long* d, int iters) {
   double avg = 0;
   for (int i = 0; i < sms; ++i) avg += double(h[i]);
   avg /= sms;
-  printf("%s N=%3d: %.1f cycles/MMA (nominal %d) %s\n", TS ? "TS" : "SS", N, avg / iters, 128 * N / 256,
+  printf("%s N=%3d A %s B %s: %.1f cycles/MMA (nominal %d) %s\n", TS ? "TS" : "SS", N, AMN ? "MN" : "K ",
+         BMN ? "MN" : "K ", avg / iters, 128 * N / 256,
          e == cudaSuccess ? "" : cudaGetErrorString(e));
 }
 
@@ -72,5 +78,10 @@ int main() {
   run<64, true>(sms, d, iters);
   run<128, true>(sms, d, iters);
   run<256, true>(sms, d, iters);
+  run<64, false, 1, 1>(sms, d, iters);   // dQ^T = K^T dS^T in the backward
+  run<64, false, 0, 1>(sms, d, iters);
+  run<64, false, 1, 0>(sms, d, iters);
+  run<128, false, 1, 1>(sms, d, iters);
+  run<128, true, 0, 1>(sms, d, iters);   // dV += P^T dO (A in TMEM, B MN-major)
   return 0;
 }
