@@ -295,13 +295,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         ZP_BITEM(3, (unsigned long long)n_steps);
       }
 #endif
-      auto issue_sdp = [&](int m) {
+      // dP^T(m): its buffer was released by dK(m-2), which precedes it in issue order
+      auto issue_dp = [&](int m) {
         const int buf = m & 1, qs = m % kQStages;
         if (lane == 0 && m < 256) ZP_BSTAMP(3072 + m * 4 + 0);
         mbar_wait(bar(B_QDO_FULL + qs), (m / kQStages) & 1);
         if (lane == 0 && m < 256) ZP_BSTAMP(3072 + m * 4 + 1);
-        // dP^T(m) first: its buffer was released by dK(m-2), which precedes it
-        // in issue order, so it overlaps the drain of dQ^T(m-2) that S^T(m) waits for
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk) {
@@ -309,7 +308,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t bo = ((kk >> 2) * kQBox + (kk & 3) * 32) >> 4;
           mma_ss_w(tDP0 + 64 * buf, v_kmaj + ao, do_kmaj + q_step * qs + bo, idesc_t, kk > 0 ? 1u : 0u);
         }
-        if (m >= 2) mbar_wait(bar(B_DQ_EMPTY + buf), ((m >> 1) - 1) & 1);  // dQ^T(m-2) drained
+      };
+      // S^T(m) once dQ^T(m-2) has drained from its columns, then SDP_FULL(m)
+      auto issue_s = [&](int m) {
+        const int buf = m & 1, qs = m % kQStages;
+        if (m >= 2) mbar_wait(bar(B_DQ_EMPTY + buf), ((m >> 1) - 1) & 1);
         if (lane == 0 && m < 256) ZP_BSTAMP(3072 + m * 4 + 2);
         tc_fence_after();
 #pragma unroll
@@ -321,9 +324,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_commit_w(bar(B_SDP_FULL + buf));
         if (lane == 0 && m < 256) ZP_BSTAMP(3072 + m * 4 + 3);
       };
-      if (n_steps > 0) issue_sdp(0);
+      if (n_steps > 0) {
+        issue_dp(0);
+        issue_s(0);
+      }
       for (int n = 0; n < n_steps; ++n) {
-        if (n + 1 < n_steps) issue_sdp(n + 1);
+        if (n + 1 < n_steps) {
+          issue_dp(n + 1);
+          issue_s(n + 1);
+        }
         const int buf = n & 1, qs = n % kQStages;
         mbar_wait(bar(B_PDS_FULL + buf), (n >> 1) & 1);
         tc_fence_after();
