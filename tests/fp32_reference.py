@@ -50,6 +50,50 @@ def causal_attention_fp32(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, sca
     return o, lse
 
 
+def causal_attention_backward_fp32(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, dout: torch.Tensor,
+                                   scale: float | None = None, block: int = 256
+                                   ) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """Gradients of ``causal_attention_fp32`` for one whole sequence, in
+    plain fp32 (TF32 off), blockwise over query rows: the reference's own O
+    and LSE, Delta = rowsum(dO * O), then per query block P = exp(S - LSE),
+    dS = P * (dO V^T - Delta), dQ = scale * dS K, dK += scale * dS^T Q,
+    dV += P^T dO.  Returns (dq [n, Hq, d], dk, dv [n, Hkv, d]) fp32."""
+    n, hq, d = q.shape
+    hkv = k.shape[1]
+    g = hq // hkv
+    scale = d ** -0.5 if scale is None else scale
+    o, lse = causal_attention_fp32(q, k, v, scale, block)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        kf = k.float().permute(1, 0, 2).contiguous()   # [hkv, n, d]
+        vf = v.float().permute(1, 0, 2).contiguous()
+        delta = (dout.float() * o).sum(-1).transpose(0, 1).contiguous()  # [hq, n]
+        dq = torch.empty(n, hq, d, dtype=torch.float32, device=q.device)
+        dk = torch.zeros(hkv, n, d, dtype=torch.float32, device=q.device)
+        dv = torch.zeros(hkv, n, d, dtype=torch.float32, device=q.device)
+        for c0 in range(0, n, block):
+            c1 = min(n, c0 + block)
+            m = c1 - c0
+            # [hkv, g*m, d]: row j*m + i = query row c0+i of head kvh*g + j
+            grp = lambda t: t[c0:c1].float().view(m, hkv, g, d).permute(1, 2, 0, 3).reshape(hkv, g * m, d)  # noqa: E731
+            qc, doc = grp(q), grp(dout)
+            s = torch.bmm(qc, kf[:, :c1].transpose(1, 2)).mul_(scale).view(hkv, g, m, c1)
+            diag = torch.ones(m, m, dtype=torch.bool, device=q.device).triu_(1)  # key > query
+            s[..., c0:c1].masked_fill_(diag, float("-inf"))
+            p = torch.exp(s.sub_(lse[:, c0:c1].reshape(hkv, g, m, 1))).view(hkv, g * m, c1)
+            del s
+            dp = torch.bmm(doc, vf[:, :c1].transpose(1, 2))                     # [hkv, g*m, c1]
+            dp.sub_(delta[:, c0:c1].reshape(hkv, g * m, 1)).mul_(p)             # dS
+            dq[c0:c1] = (torch.bmm(dp, kf[:, :c1]) * scale).view(hkv, g, m, d).permute(2, 0, 1, 3).reshape(m, hq, d)
+            dk[:, :c1] += torch.bmm(dp.transpose(1, 2), qc) * scale
+            dv[:, :c1] += torch.bmm(p.transpose(1, 2), doc)
+            del p, dp
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return dq, dk.permute(1, 0, 2).contiguous(), dv.permute(1, 0, 2).contiguous()
+
+
 class ErrorStats:
     """Accumulates the north-star error measures of an output against the
     fp32 reference: max |o - r|, mean-rel = sum |o - r| / sum |r|,
