@@ -229,10 +229,6 @@ class HeadAdapter:
     def identity(self) -> bool:
         return self.d == HEAD_DIM and self.dup == 1
 
-    @property
-    def kernel_heads(self) -> int:
-        return self.hq * self.dup
-
     def inputs(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor):
         pad = HEAD_DIM - self.d
         if pad:

@@ -129,14 +129,6 @@ class RankProgram:
     # rank (cuts[-1] before the first); the rest after the last ring
     local_cuts: list[int] = field(default_factory=list)
 
-    @property
-    def max_held_rows(self) -> int:
-        return max((max(r.held_rows) for r in self.rings), default=0)
-
-    @property
-    def max_state_rows(self) -> int:
-        return max((r.state_rows for r in self.rings), default=0)
-
     def pairs_per_head(self) -> int:
         return self.local.pairs_per_head + sum(rr.work.pairs_per_head for r in self.rings for rr in r.rounds)
 
