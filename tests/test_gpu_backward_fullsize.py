@@ -78,15 +78,16 @@ def test_backward_full_c2_batch_matches_fp32():
         assert st["max_abs"] <= TOL_REL * st["max_ref"] + TOL_ABS, (name, st)
 
 
-def test_ring_backward_c3_g2_matches_fp32():
-    """Config 3 at G=2 (one 2-position ring holding the 131,072-token
-    sequence): both ranks emulated on one GPU through the production forward
+@pytest.mark.parametrize("gpus", [2, 4, 8])
+def test_ring_backward_c3_matches_fp32(gpus):
+    """Config 3 at G=2/4/8 (the 131,072-token sequence in a ring; at G=8 five
+    rings): every rank emulated on one GPU through the production forward
     and backward executors (ring rounds, KV hops, travelling dK/dV totals),
     gradients gathered per sequence against the chunked fp32 backward."""
     from paper_2509_21841_b200 import plan as P, schedule as S
     from paper_2509_21841_b200.emulate import emulate_backward_on_one_gpu, emulate_ranks_on_one_gpu
-    batch = W.c3_batch(2)
-    plan = P.build_plan(batch, W.cluster_for(batch, 2))
+    batch = W.c3_batch(gpus)
+    plan = P.build_plan(batch, W.cluster_for(batch, gpus))
     assert plan.ring_groups
     sched = S.build_schedule(plan)
     seqs = sorted(plan.sequence_lengths.items())
@@ -114,6 +115,6 @@ def test_ring_backward_c3_g2_matches_fp32():
             a[3] += ref[j].double().abs().sum().item()
         del ref
     stats = {name: {"max_abs": e, "max_ref": m, "mean_rel": es / rs} for name, (e, m, es, rs) in acc.items()}
-    _record("ring_backward_c3_g2", stats)
+    _record(f"ring_backward_c3_g{gpus}", stats)
     for name, st in stats.items():
         assert st["max_abs"] <= TOL_REL * st["max_ref"] + TOL_ABS, (name, st)
