@@ -131,6 +131,8 @@ struct AttnArgs {
   int hq;
   int group;  // hq / hkv
   float scale_log2;
+  int q_rows;   // bounds of q / o and k / v (checked in -DZP_CHECKS builds)
+  int kv_rows;
 };
 
 // Walks the KV tiles an item needs, in order: tiles of each segment up to the
@@ -416,6 +418,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (u.idx >= n_units) break;
         const zp_attn_item it = u.item;
         if (u.n_tiles == 0) continue;
+        ZP_CHECK(it.q_len >= 1 && it.q_len <= kBM && it.q_row0 >= 0 && it.q_row0 + it.q_len <= args.q_rows,
+                 "fwd item q rows", it.q_row0, it.q_len);
+        ZP_CHECK(it.q_row0 + it.q_len <= args.lse_stride, "fwd item lse row", it.q_row0 + it.q_len, args.lse_stride);
+        ZP_CHECK(2 * it.head_pair + 1 < args.hq, "fwd item head pair", it.head_pair, args.hq);
+        ZP_CHECK(!(it.flags & (ZP_ITEM_LOAD_STATE | ZP_ITEM_STORE_STATE)) ||
+                     (args.st_o != nullptr && it.state_row0 >= 0 && it.state_row0 + it.q_len <= args.state_rows),
+                 "fwd item state rows", it.state_row0, args.state_rows);
         const int kvh = (2 * it.head_pair) / args.group;
         // Q of head tile t, once that head's last QK^T of the previous item is done
         auto load_q = [&](int t) {
@@ -436,6 +445,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int kst = int(jg % C::kKStages), vst = int(jg % C::kVStages);
           const uint32_t ku = jg / C::kKStages, vu = jg / C::kVStages;
           const int row = cur.row();
+          ZP_CHECK(cur.g.row0 >= 0 && cur.g.len >= 0 && cur.g.row0 + cur.g.len <= args.kv_rows, "fwd kv segment",
+                   cur.g.row0, cur.g.len);
           if (jg >= uint32_t(C::kKStages)) mbar_wait(bar(B_KEMPTY + kst), (ku - 1) & 1);
           if (cta == 0) mbar_expect_tx(bar(B_KFULL + kst), (kPair ? 2 : 1) * C::kKBytes);
           for (int b = 0; b < 2; ++b) {
@@ -982,6 +993,8 @@ int attn_fwd_common(bool parity, const void* q, const void* k, const void* v, in
   a.state_rows = state_rows;
   a.hq = hq;
   a.group = hq / hkv;
+  a.q_rows = q_rows;
+  a.kv_rows = kv_rows;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t me = cudaMemsetAsync(workspace, 0, sizeof(int), s);

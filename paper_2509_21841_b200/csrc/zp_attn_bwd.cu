@@ -94,6 +94,8 @@ struct BwdArgs {
   int group;
   float scale;
   float scale_log2;
+  int q_rows;   // bounds of q / dO / dq and k / v / dk / dv (checked in -DZP_CHECKS builds)
+  int kv_rows;
 };
 
 template <bool B>
@@ -203,6 +205,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const zp_bwd_item it = args.items[blockIdx.x];
+  ZP_CHECK(it.kv_len >= 1 && it.kv_len <= kBK && it.kv_row0 >= 0 && it.kv_row0 + it.kv_len <= args.kv_rows,
+           "bwd item kv rows", it.kv_row0, it.kv_len);
+  ZP_CHECK(it.kv_head >= 0 && it.kv_head < args.hkv, "bwd item kv head", it.kv_head, args.hkv);
 #ifdef ZP_TRACE
   if (threadIdx.x == 0) ZP_BITEM(0, gtimer());
 #endif
@@ -251,6 +256,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (n >= uint32_t(kQStages)) mbar_wait(bar(B_QDO_EMPTY + qs), ((n / kQStages) - 1) & 1);
         mbar_expect_tx(bar(B_QDO_FULL + qs), 2 * kQTile);
         const int h = kvh * args.group + cur.hh;
+        ZP_CHECK(cur.g.row0 >= 0 && cur.g.row0 + cur.g.len <= args.q_rows && cur.g.row0 + cur.g.len <= args.lse_stride,
+                 "bwd q segment", cur.g.row0, cur.g.len);
         for (int b = 0; b < 2; ++b) {
           tma_load_2d(sbase + kSmemQ + qs * kQTile + b * kQBox, &tm_q, bar(B_QDO_FULL + qs), h * kD + b * 64,
                       cur.row(), pol_q);
@@ -659,6 +666,8 @@ extern "C" int zp_attn_bwd(const void* q, const void* k, const void* v, const vo
   a.hq = hq;
   a.hkv = hkv;
   a.group = hq / hkv;
+  a.q_rows = q_rows;
+  a.kv_rows = kv_rows;
   a.scale = softmax_scale;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
   attn_bwd_kernel<<<n_items, kThreads, kSmemBytes, reinterpret_cast<cudaStream_t>(stream)>>>(tq, tdo, tk, tv, tdq,

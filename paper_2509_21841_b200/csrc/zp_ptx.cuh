@@ -7,6 +7,25 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
+// Diagnostic build only (-DZP_CHECKS): bounds checks at the kernels' direct
+// global accesses and on every work item they consume.  A violation prints
+// the site and traps (the pool does not allow compute-sanitizer).
+#ifdef ZP_CHECKS
+#include <cstdio>
+#define ZP_CHECK(cond, what, a, b)                                                                   \
+  do {                                                                                                \
+    if (!(cond)) {                                                                                    \
+      printf("ZP_CHECK failed: %s (%lld, %lld) block %d thread %d\n", what, (long long)(a), (long long)(b), \
+             int(blockIdx.x), int(threadIdx.x));                                                      \
+      __trap();                                                                                       \
+    }                                                                                                 \
+  } while (0)
+#else
+#define ZP_CHECK(cond, what, a, b) \
+  do {                             \
+  } while (0)
+#endif
+
 namespace zp {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
